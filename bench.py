@@ -1,0 +1,419 @@
+"""Benchmark: kernel configurations evaluated per second (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): the range-four 3D25pt
+star stencil on a 640^3 grid, full block-size sweep — every power-of-two
+block (X, Y <= 512, Z <= 64) with X*Y*Z <= 1024 threads, 264 shapes of which
+246 tile the grid (skip_invalid) — evaluated with the B200 machine
+parameters, default fits, block_samples=5, wave_samples=2, then ranked.
+A step = evaluate + rank the whole sweep.  With N GPUs each rank evaluates
+its own 246-config shard (the same sweep with field alignment 8*rank bytes,
+so every rank's configs are distinct), records are all-gathered over NCCL
+and the global ranking runs on the device (weak scaling).
+
+--impl reference times the reference's own CPU estimator (pip-installed
+unmodified under baseline/_ref; the CPU oracle port if that is missing) on a
+bounded sample of the same workload with all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+GRID = (640, 640, 640)
+RADIUS = 4
+# kernels per step: setup, warp stats, interval sets, assembly (one batch)
+# + rank: keys, 2 x 8 digit passes x (hist, scan, scatter), gather, output
+LAUNCHES_PER_STEP = 4 + 1 + 48 + 1 + 1
+
+
+def sweep_configs():
+    from paper_2107_01143_b200 import gvo
+
+    out = []
+    t = 1
+    while t <= 1024:
+        out.extend(gvo.enumerate_sweep(t))
+        t *= 2
+    return out
+
+
+def b200_machine():
+    from paper_2107_01143_b200 import gvo
+
+    return gvo.b200_preset()
+
+
+# ---------------------------------------------------------------- device arm
+def build_shard(rank: int):
+    """Device config records of this rank's shard + template bookkeeping."""
+    from dataclasses import replace
+
+    from paper_2107_01143_b200 import gvo
+    from paper_2107_01143_b200.gvo import _engine
+
+    fam = gvo.KernelFamily("stencil", GRID, radius=RADIUS)
+    m = b200_machine()
+    batch = _engine.Batch()
+    kept = []
+    base = None
+    for cfg in sweep_configs():
+        try:
+            launch, flops = fam.launch_of(cfg)
+        except ValueError:
+            continue
+        if base is None:
+            k = fam.build(cfg)
+            fields = tuple(replace(f, alignment=8 * rank) for f in k.fields)
+            base = (fields, k.accesses)
+        batch.add(base[0], base[1], launch, flops, m, None, _engine.FOLD_RANK[cfg.folding])
+        kept.append(cfg)
+    return batch, kept
+
+
+def n_addr(cfg_launch, n_acc: int, m) -> int:
+    """Brute-force address-granule evaluations the reference performs for one
+    config: blocks n_b*T*A (+ lines), L1 T*A, waves U*B_w*T*A."""
+    t = cfg_launch.threads_per_block
+    per_sm = min(m.max_blocks_per_sm, m.max_threads_per_sm // t)
+    bw = m.sm_count * per_sm
+    total = cfg_launch.total_blocks
+    nw = -(-total // bw)
+    u = 1 if nw == 1 else 3
+    n_b = min(5, max(1, (cfg_launch.grid_dim[0] - 2) * (cfg_launch.grid_dim[1] - 2) * (cfg_launch.grid_dim[2] - 2)))
+    return n_b * t * n_acc + t * n_acc + u * min(bw, total) * t * n_acc
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples)
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[2:]) if v.lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.samples[0][1]), "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_sample_rate(configs_for_cpu, seconds_target=20.0):
+    """Reference CPU estimator on a bounded sample (multiprocessing pool)."""
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0))
+    n = max(cores, 8)
+    rng = np.random.default_rng(20240811)
+    pick = [configs_for_cpu[i] for i in rng.choice(len(configs_for_cpu), size=min(n, len(configs_for_cpu)),
+                                                     replace=False)]
+    kind = _ref_kind()
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(min(cores, len(pick))) as pool:
+        pool.map(_cpu_eval, [(kind, c) for c in pick])
+    dt = time.perf_counter() - t0
+    return {"value": len(pick) / dt, "unit": "configs/s", "cores": min(cores, len(pick)), "kind": kind,
+            "sample": f"{len(pick)} seeded-random configs of the 246-config C2 sweep, "
+                      f"reference evaluate_kernel (B200 params, samples 5/2), {dt:.1f} s"}
+
+
+def _ref_kind():
+    return "reference" if (ROOT / "baseline" / "_ref" / "gvo").exists() else "port"
+
+
+def _cpu_eval(arg):
+    kind, key = arg
+    bx, by, bz = (int(v) for v in key.split("/")[0].split("x"))
+    if kind == "reference":
+        sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
+        import dataclasses
+
+        import gvo as ref
+
+        m = dataclasses.replace(ref.v100_preset(), name="b200", sm_count=148, clock_ghz=1.965,
+                                l1_capacity_bytes=256 * 1024, l2_capacity_bytes=126 * 1024 * 1024,
+                                mem_bandwidth_gbps=6531.3, l2_bandwidth_gbps=20000.0)
+        k = ref.KernelFamily("stencil", GRID, radius=RADIUS).build(ref.SweepConfig((bx, by, bz)))
+        return ref.evaluate_kernel(k, m).glups
+    from oracle import gvo_oracle as ora
+    from paper_2107_01143_b200 import gvo
+
+    k = gvo.KernelFamily("stencil", GRID, radius=RADIUS).build(gvo.SweepConfig((bx, by, bz)))
+    return ora.evaluate_kernel(k, b200_machine())["glups"]
+
+
+def run_device(args, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2107_01143_b200 import _native
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    ctx = _native.context()
+    L = _native.lib()
+    batch, kept = build_shard(rank)
+    cfg_np = batch.config_array()
+    n = len(cfg_np)
+    ctx.sync_registries()
+    F = ctx.max_fields
+    S, W = _native.effective_sampling(5, 2)
+    smp = _native.Sampling(5, 2, 0, 7, 0)
+    stride = _native.counts_stride(F, S, W)
+    d_cfgs = torch.from_numpy(cfg_np.view(np.uint8).copy()).to(dev)
+    d_counts = torch.zeros((n, stride), dtype=torch.int64, device=dev)
+    d_stats = torch.zeros((n, _native.stats_len(F)), dtype=torch.float64, device=dev)
+    d_rec = torch.zeros((n, _native.RECORD_LEN), dtype=torch.float64, device=dev)
+    d_order = torch.zeros(n * world, dtype=torch.int64, device=dev)
+    if world > 1:
+        g_rec = torch.zeros((n * world, _native.RECORD_LEN), dtype=torch.float64, device=dev)
+        g_cfgs = torch.zeros(n * world * cfg_np.itemsize, dtype=torch.uint8, device=dev)
+        dist.all_gather_into_tensor(g_cfgs, d_cfgs)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    C = _native.C
+
+    def step():
+        ctx.check(L.gvo_eval_configs(ctx.h, C.c_void_p(d_cfgs.data_ptr()), n, C.byref(smp), F,
+                                     C.c_void_p(d_counts.data_ptr()), C.c_void_p(d_stats.data_ptr()),
+                                     C.c_void_p(d_rec.data_ptr()), None, None, 0, C.c_void_p(sp)))
+        if world > 1:
+            dist.all_gather_into_tensor(g_rec, d_rec)
+            ctx.check(L.gvo_rank(ctx.h, C.c_void_p(g_rec.data_ptr()), C.c_void_p(g_cfgs.data_ptr()), n * world,
+                                 C.c_void_p(d_order.data_ptr()), C.c_void_p(sp)))
+        else:
+            ctx.check(L.gvo_rank(ctx.h, C.c_void_p(d_rec.data_ptr()), C.c_void_p(d_cfgs.data_ptr()), n,
+                                 C.c_void_p(d_order.data_ptr()), C.c_void_p(sp)))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    status = d_counts[:, _native.C_STATUS].cpu().numpy()
+    assert (status == 0).all(), f"engine status {np.unique(status)}"
+    L.gvo_set_timing(ctx.h, 1)
+    L.gvo_kernel_times(ctx.h, None, None, 1)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)  # > L2: evict between timed steps
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    kms = (C.c_double * 8)()
+    kcnt = (C.c_int64 * 8)()
+    L.gvo_kernel_times(ctx.h, kms, kcnt, 1)
+    L.gvo_set_timing(ctx.h, 0)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = n * world * args.steps / (ms_max * 1e-3)
+
+    # ---- e2e through the C ABI with host buffers (copies inside the region)
+    counts_h = np.zeros((n, stride), dtype=np.int64)
+    stats_h = np.zeros((n, _native.stats_len(F)), dtype=np.float64)
+    rec_h = np.zeros((n, _native.RECORD_LEN), dtype=np.float64)
+    e2e_steps = max(3, args.steps // 2)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ctx.check(L.gvo_eval_configs_host(ctx.h, _native._ptr(cfg_np), n, C.byref(smp), F, _native._ptr(counts_h),
+                                          _native._ptr(stats_h), _native._ptr(rec_h), None, None, 0))
+        rec_d = torch.from_numpy(rec_h).to(dev, non_blocking=False)
+        if world > 1:
+            dist.all_gather_into_tensor(g_rec, rec_d)
+            ctx.check(L.gvo_rank(ctx.h, C.c_void_p(g_rec.data_ptr()), C.c_void_p(g_cfgs.data_ptr()), n * world,
+                                 C.c_void_p(d_order.data_ptr()), C.c_void_p(sp)))
+        else:
+            ctx.check(L.gvo_rank(ctx.h, C.c_void_p(rec_d.data_ptr()), C.c_void_p(d_cfgs.data_ptr()), n,
+                                 C.c_void_p(d_order.data_ptr()), C.c_void_p(sp)))
+        order_h = d_order.cpu().numpy()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = n * world * e2e_steps / float(te.item())
+    h2d = n * cfg_np.itemsize + n * _native.RECORD_LEN * 8
+    d2h = n * stride * 8 + n * _native.stats_len(F) * 8 + n * _native.RECORD_LEN * 8 + n * world * 8
+    del order_h
+
+    if rank != 0:
+        return
+    # ---- roofline: dominant kernel (interval-union engine) vs measured INT32 issue rate
+    names = ("setup", "warp", "sets", "finish", "rank")
+    kernel_ms = {names[i]: kms[i] / max(1, args.steps) for i in range(5)}
+    top = max(("setup", "warp", "sets", "finish"), key=lambda k: kernel_ms[k])
+    peak = C.c_double()
+    ctx.check(L.gvo_int_peak(ctx.h, C.byref(peak)))
+    m = b200_machine()
+    fam_acc = 26
+    n_addr_total = 0
+    from paper_2107_01143_b200 import gvo as G
+
+    fam = G.KernelFamily("stencil", GRID, radius=RADIUS)
+    for cfg in kept:
+        launch, _ = fam.launch_of(cfg)
+        n_addr_total += n_addr(launch, fam_acc, m)
+    k_int = 8
+    sets_s = kernel_ms["sets"] * 1e-3
+    achieved = k_int * n_addr_total / sets_s / 1e9
+    algo_bytes = n * (cfg_np.itemsize + stride * 8 + _native.stats_len(F) * 8 + _native.RECORD_LEN * 8)
+    cpu = cpu_sample_rate([c.key for c in kept]) if world == 1 and not args.no_cpu else None
+    line = {
+        "metric": "kernel configs evaluated/sec (1/2/4/8 B200) vs host-CPU reference; % int/HBM roofline",
+        "value": value, "unit": "configs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int64", "data": "synthetic (deterministic config-space enumeration)",
+        "config": {"workload": "C2: 3D25pt r4 640^3 full power-of-two block sweep (246 valid configs/rank), "
+                               "B200 machine params, samples 5/2, evaluate+rank",
+                   "configs_per_rank": n, "parallelism": f"dp{world} (config shards, NCCL all-gather + device rank)",
+                   "l2": "flushed between timed steps (256 MiB write)"},
+        "e2e": {"value": e2e_value, "unit": "configs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(args.steps * LAUNCHES_PER_STEP),
+        "kernel_ms_per_step": kernel_ms,
+        "roofline": {"bound": "int", "kernel": "k_sets (interval-union engine)",
+                     "achieved": achieved, "peak": peak.value / 1e9, "unit": "Gop/s (int32, address-equivalent)",
+                     "frac": achieved / (peak.value / 1e9),
+                     "note": "achieved = 8 int ops x brute-force address-granules the reference enumerates "
+                             "(SURVEY §8d N_addr) / k_sets time; >1 means the lattice collapse does less work "
+                             "than enumeration. peak = measured INT32 issue rate (gvo_int_peak).",
+                     "hbm": {"achieved": algo_bytes / (ms_step * 1e-3) / 1e9, "peak": 6531.3, "unit": "GB/s",
+                             "frac": algo_bytes / (ms_step * 1e-3) / 1e9 / 6531.3},
+                     "traffic": None},
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0))
+    keys = [c.key for c in _valid_cfgs()]
+    kind = _ref_kind()
+    rng = np.random.default_rng(20240811)
+    per_step = max(cores, 8)
+    times = []
+    with mp.get_context("spawn").Pool(cores) as pool:
+        for i in range(args.warmup + args.steps):
+            pick = [keys[j] for j in rng.choice(len(keys), size=min(per_step, len(keys)), replace=False)]
+            t0 = time.perf_counter()
+            pool.map(_cpu_eval, [(kind, k) for k in pick])
+            if i >= args.warmup:
+                times.append((len(pick), time.perf_counter() - t0))
+    n_done = sum(a for a, _ in times)
+    secs = sum(b for _, b in times)
+    value = n_done / secs
+    line = {
+        "impl": "reference",
+        "metric": "kernel configs evaluated/sec (1/2/4/8 B200) vs host-CPU reference; % int/HBM roofline",
+        "value": value, "unit": "configs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": secs / len(times) * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int64", "data": "synthetic (deterministic config-space enumeration)",
+        "config": {"workload": "C2: 3D25pt r4 640^3 full power-of-two block sweep, B200 params, samples 5/2",
+                   "per_step_sample": per_step},
+        "cpu_baseline": {"value": value, "unit": "configs/s", "cores": cores, "kind": kind,
+                         "sample": f"{per_step} seeded-random configs per step of the 246-config sweep"},
+        "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _valid_cfgs():
+    from paper_2107_01143_b200 import gvo
+
+    fam = gvo.KernelFamily("stencil", GRID, radius=RADIUS)
+    out = []
+    for c in sweep_configs():
+        try:
+            fam.launch_of(c)
+            out.append(c)
+        except ValueError:
+            pass
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the in-run CPU baseline")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    try:
+        run_device(args, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,66 @@
+// gvo_kernels.h — host-side launchers of the device pipeline (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include "gvo_common.cuh"
+
+namespace gvo {
+
+// dynamic shared memory of the set kernel (2 CTAs per SM)
+constexpr int kSetsSmemBytes = 112 * 1024;
+
+void launch_setup(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs,
+                  int64_t n, const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos,
+                  cudaStream_t st);
+
+void launch_warp(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs, const Geo* d_geos, const int64_t* d_coefs,
+                 int64_t n_items, int S_req, int64_t sector, int64_t bank_width, int64_t n_banks,
+                 int mode, const int64_t* d_block_list, int64_t* d_counts, int64_t counts_stride,
+                 int F_stride, int64_t* d_l1_access, int32_t l1_stride, unsigned long long* d_out,
+                 int max_acc, int n_sm, cudaStream_t st);
+
+struct SetsLaunch {
+  TplView T;
+  const gvo_machine* machines;
+  const gvo_config* cfgs;
+  const Geo* geos;
+  const int64_t* coefs;
+  int64_t n_items;
+  int S_req;
+  int F_stride;
+  int mode;
+  int64_t granularity;
+  const int64_t* run_start;
+  const int64_t* run_count;
+  int n_custom_runs;
+  int64_t* counts;
+  int64_t counts_stride;
+  uint8_t* slab;
+  int64_t slab_bytes;
+  int64_t run_cap;
+  int64_t elem_cap;
+  int* status_out;
+  int n_ctas;
+};
+void launch_sets(const SetsLaunch& L, cudaStream_t st);
+int64_t sets_slab_bytes(int64_t run_cap, int64_t elem_cap);
+
+// float assembly + prediction (k_assemble.cu)
+void launch_finish(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs,
+                   const Geo* d_geos, int64_t n, int S_req, int W_req, int F, int64_t* d_counts,
+                   int64_t counts_stride, double* d_stats, double* d_records, double* d_field_down,
+                   cudaStream_t st);
+void launch_assemble_stats(const gvo_machine* d_machines, const int32_t* d_mid, const int64_t* d_flops,
+                           int64_t n, int F, const double* d_stats, double* d_records,
+                           double* d_field_down, cudaStream_t st);
+
+void launch_predict(const gvo_machine* d_machines, const int32_t* d_mid, const double* dd, const double* ld,
+                    const double* cyc, const int64_t* fl, int64_t n, double* out, cudaStream_t st);
+
+int launch_int_peak(int n_sm, cudaStream_t st, double* ops_per_s);
+
+// ranking (k_rank.cu)
+int64_t rank_scratch_bytes(int64_t n);
+void launch_rank(const double* d_records, const gvo_config* d_cfgs, int64_t n, int64_t* d_order,
+                 void* d_scratch, cudaStream_t st);
+
+}  // namespace gvo

@@ -1,0 +1,760 @@
+// k_sets.cu — exact unique-granule counting for blocks and waves.
+//
+// Replaces the reference's set machinery: GranuleSet/_SetBuilder bitmaps and
+// sorted-unique arrays (footprint.py:141-227), grid_iteration's unique
+// counts (footprint.py:441-471), wave_footprint / overlap_bytes
+// (footprint.py:535-584) and the unique counts of sample_block_stats /
+// sample_wave_stats (volumes.py:152-250).
+//
+// Instead of materialising every address, each (access, block box) is an
+// affine image of a box of thread/block coordinates.  Its dimensions are
+// collapsed like a strided tensor (contiguous strides merge), the innermost
+// dimensions whose gaps never exceed one granule fold into a byte "span",
+// and accesses that differ only by a translation along a remaining
+// dimension (stencil rays) or by less than span+granule (clusters) merge
+// into one lattice.  Each lattice point then contributes one granule
+// INTERVAL.  All intervals of a unit (one field of one block, or one field
+// over all sampled waves, loads and stores tagged separately) are radix
+// sorted by their first granule in shared memory (or a per-CTA global slab
+// when they do not fit) and every requested union / intersection count is
+// a tagged prefix-max sweep.  Every step is an exact set identity; no
+// address sampling, no hashing.
+#include "gvo_bytecode.cuh"
+#include "gvo_kernels.h"
+
+namespace gvo {
+
+constexpr int kNT = 512;           // threads per CTA
+constexpr int kNW = kNT / 32;
+constexpr int kMaxSrc = 64;        // sources per unit
+constexpr int kMaxSub = 72;        // subsets per unit
+constexpr int kSmemRuns = 1024;    // run offsets kept in shared memory
+constexpr int kClassPts = 64;      // points per coefficient class chunk
+
+struct UnitSh {
+  int64_t cfg;
+  int field;
+  int kind;      // 0 block sample, 1 waves, 2 custom footprint
+  int j;         // sample index (kind 0)
+  int n_src;
+  int64_t src_start[kMaxSrc], src_count[kMaxSrc];
+  int src_kind[kMaxSrc], src_tag[kMaxSrc];
+  int n_sub;
+  uint32_t sub_mask[kMaxSub];
+  int64_t sub_r[kMaxSub];
+  int64_t sub_val[kMaxSub];
+  int64_t g, R;
+  int status;
+  int n_runs;
+  int64_t key_lo, key_hi;  // granule bounds over all runs
+  int64_t N;
+};
+
+// ------------------------------------------------------------------ lattice
+struct Lat {
+  int64_t base;
+  uint64_t span;
+  int nd;
+  uint64_t st[kMaxDims];
+  int64_t ex[kMaxDims];
+};
+
+__device__ inline void sort_dims(Lat& L) {
+  for (int i = 1; i < L.nd; ++i) {
+    uint64_t s = L.st[i];
+    int64_t e = L.ex[i];
+    int k = i - 1;
+    while (k >= 0 && L.st[k] > s) { L.st[k + 1] = L.st[k]; L.ex[k + 1] = L.ex[k]; --k; }
+    L.st[k + 1] = s;
+    L.ex[k + 1] = e;
+  }
+}
+
+// merge dims whose union is again an arithmetic progression, then fold the
+// leading dims whose point gaps stay <= g into the granule-contiguous span.
+__device__ inline void normalize(Lat& L, int64_t g) {
+  sort_dims(L);
+  int m = 0;
+  for (int i = 0; i < L.nd; ++i) {
+    if (L.ex[i] <= 1 || L.st[i] == 0) continue;
+    if (m > 0) {
+      const uint64_t sc = L.st[m - 1];
+      const int64_t sn = L.ex[m - 1];
+      if (L.st[i] % sc == 0 && L.st[i] / sc <= (uint64_t)sn) {
+        L.ex[m - 1] = sn + (int64_t)(L.st[i] / sc) * (L.ex[i] - 1);
+        continue;
+      }
+    }
+    L.st[m] = L.st[i];
+    L.ex[m] = L.ex[i];
+    ++m;
+  }
+  L.nd = m;
+  int k = 0;
+  while (k < L.nd && (unsigned __int128)L.st[k] <= (unsigned __int128)L.span + (uint64_t)g) {
+    L.span += L.st[k] * (uint64_t)(L.ex[k] - 1);
+    ++k;
+  }
+  if (k) {
+    for (int i = k; i < L.nd; ++i) { L.st[i - k] = L.st[i]; L.ex[i - k] = L.ex[i]; }
+    L.nd -= k;
+  }
+}
+
+__device__ inline bool contains(const int64_t* P, int n, int64_t v) {
+  int lo = 0, hi = n - 1;
+  while (lo <= hi) {
+    int mid = (lo + hi) >> 1;
+    if (P[mid] == v) return true;
+    if (P[mid] < v) lo = mid + 1; else hi = mid - 1;
+  }
+  return false;
+}
+
+struct RunSink {
+  Run* runs;
+  int cap;
+  int* n_runs;
+  int* status;
+  int64_t* key_lo;
+  int64_t* key_hi;
+};
+
+__device__ inline void emit_lattice(const RunSink& S, Lat L, int tag, const Granule& G) {
+  normalize(L, G.g);
+  int64_t count = 1;
+  uint64_t ext_span = L.span;
+  for (int d = 0; d < L.nd; ++d) {
+    if (count > (int64_t(1) << 40) / L.ex[d]) { atomicExch(S.status, GVO_ERR_CAPACITY); return; }
+    count *= L.ex[d];
+    ext_span += L.st[d] * (uint64_t)(L.ex[d] - 1);
+  }
+  const int64_t len = (int64_t)(L.span / (uint64_t)G.g) + 2;
+  const int64_t pieces = (len + kPiece - 1) / kPiece;
+  const int slot = atomicAdd(S.n_runs, 1);
+  if (slot >= S.cap) { atomicExch(S.status, GVO_ERR_CAPACITY); return; }
+  Run r;
+  r.base = L.base;
+  r.span = L.span;
+  r.nd = L.nd;
+  for (int d = 0; d < kMaxDims; ++d) { r.stride[d] = d < L.nd ? (int64_t)L.st[d] : 0; r.ext[d] = d < L.nd ? L.ex[d] : 1; }
+  r.tag = tag;
+  r.kind = 0;
+  r.access = -1;
+  r.pieces = pieces;
+  r.count = count * pieces;
+  r.run_start = r.run_count = 0;
+  S.runs[slot] = r;
+  atomicMin((long long*)S.key_lo, (long long)G.of(L.base));
+  atomicMax((long long*)S.key_hi, (long long)G.of((int64_t)((uint64_t)L.base + ext_span)));
+}
+
+// Cover the translates P[0..n) (sorted, unique) of one lattice.  Rays along
+// an outer dimension extend that dimension; remaining points cluster when
+// consecutive gaps are <= span + g (their union keeps all gaps <= g).
+__device__ inline void cover_and_emit(const RunSink& S, const Lat& L0, const int64_t* P, int n,
+                                      int tag, const Granule& G) {
+  uint64_t req = n >= 64 ? ~0ull : ((1ull << n) - 1);
+  for (int d = L0.nd - 1; d >= 0 && req; --d) {
+    const int64_t s = (int64_t)L0.st[d];
+    for (int i = 0; i < n; ++i) {
+      if (contains(P, n, P[i] - s)) continue;  // not a ray start
+      uint64_t mem = 1ull << i;
+      int len = 1;
+      int64_t v = P[i];
+      while (true) {
+        // position of v + s
+        int lo = 0, hi = n - 1, pos = -1;
+        const int64_t t = v + s;
+        while (lo <= hi) {
+          int mid = (lo + hi) >> 1;
+          if (P[mid] == t) { pos = mid; break; }
+          if (P[mid] < t) lo = mid + 1; else hi = mid - 1;
+        }
+        if (pos < 0) break;
+        mem |= 1ull << pos;
+        ++len;
+        v = t;
+      }
+      if (len >= 2 && __popcll(mem & req) >= 2) {
+        Lat L = L0;
+        L.base = P[i];
+        L.ex[d] += len - 1;
+        emit_lattice(S, L, tag, G);
+        req &= ~mem;
+      }
+    }
+  }
+  if (!req) return;
+  // clusters over all points (covered ones act as bridges)
+  int i = 0;
+  while (i < n) {
+    int j = i;
+    uint64_t mem = 1ull << i;
+    while (j + 1 < n && (unsigned __int128)(uint64_t)(P[j + 1] - P[j]) <=
+                            (unsigned __int128)L0.span + (uint64_t)G.g) {
+      ++j;
+      mem |= 1ull << j;
+    }
+    if (mem & req) {
+      Lat L = L0;
+      L.base = P[i];
+      L.span = L0.span + (uint64_t)(P[j] - P[i]);
+      emit_lattice(S, L, tag, G);
+    }
+    i = j + 1;
+  }
+}
+
+// lattice of one coefficient vector over one block box, translation 0
+__device__ inline Lat box_lattice(const int64_t* c, const int32_t bd[3], const Box& b, const Granule& G) {
+  Lat L;
+  const int64_t ext[6] = {bd[0], bd[1], bd[2], b.n[0], b.n[1], b.n[2]};
+  uint64_t base = (uint64_t)c[4] * (uint64_t)b.lo[0] + (uint64_t)c[5] * (uint64_t)b.lo[1] +
+                  (uint64_t)c[6] * (uint64_t)b.lo[2];
+  L.nd = 0;
+  L.span = 0;
+  for (int k = 0; k < 6; ++k) {
+    int64_t co = c[1 + k];
+    if (ext[k] <= 1 || co == 0) continue;
+    if (co < 0) {
+      base += (uint64_t)co * (uint64_t)(ext[k] - 1);
+      L.st[L.nd] = (uint64_t)0 - (uint64_t)co;
+    } else {
+      L.st[L.nd] = (uint64_t)co;
+    }
+    L.ex[L.nd] = ext[k];
+    ++L.nd;
+  }
+  L.base = (int64_t)base;
+  normalize(L, G.g);
+  return L;
+}
+
+// ------------------------------------------------------------------ sort
+// CTA-wide stable LSD radix sort (8-bit digits) of packed 64-bit elements
+// on bits [bit0, bit0 + nbits).  a/b may live in shared or global memory.
+__device__ uint64_t* cta_sort(uint64_t* a, uint64_t* b, int64_t n, int bit0, int nbits,
+                              uint32_t* hist /* kNW*256 */, uint32_t* tot /* 256 */) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t chunk = (((n + kNW - 1) / kNW) + 31) & ~int64_t(31);
+  const int64_t beg = min(n, (int64_t)w * chunk), end = min(n, beg + chunk);
+  for (int sh = bit0; sh < bit0 + nbits; sh += 8) {
+    for (int i = threadIdx.x; i < kNW * 256; i += kNT) hist[i] = 0;
+    __syncthreads();
+    for (int64_t i = beg + lane; i < end; i += 32) atomicAdd(&hist[w * 256 + ((a[i] >> sh) & 255)], 1u);
+    __syncthreads();
+    if (threadIdx.x < 256) {
+      const int d = threadIdx.x;
+      uint32_t s = 0;
+      for (int k = 0; k < kNW; ++k) s += hist[k * 256 + d];
+      tot[d] = s;
+    }
+    __syncthreads();
+    if (w == 0) {  // exclusive scan of 256 digit totals, 8 per lane
+      uint32_t v[8], run = 0;
+      for (int k = 0; k < 8; ++k) { v[k] = run; run += tot[lane * 8 + k]; }
+      uint32_t incl = run;
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const uint32_t excl = incl - run;
+      for (int k = 0; k < 8; ++k) tot[lane * 8 + k] = excl + v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < 256) {
+      const int d = threadIdx.x;
+      uint32_t run = tot[d];
+      for (int k = 0; k < kNW; ++k) {
+        uint32_t h = hist[k * 256 + d];
+        hist[k * 256 + d] = run;
+        run += h;
+      }
+    }
+    __syncthreads();
+    for (int64_t i0 = beg; i0 < end; i0 += 32) {
+      const int64_t i = i0 + lane;
+      const bool v = i < end;
+      const uint64_t e = v ? a[i] : 0;
+      const uint32_t d = (uint32_t)(e >> sh) & 255u;
+      const unsigned act = __ballot_sync(0xffffffffu, v);
+      unsigned peers = 0;
+      if (v) {
+        peers = __match_any_sync(act, d);
+        const uint32_t pos = hist[w * 256 + d] + __popc(peers & ((1u << lane) - 1u));
+        b[pos] = e;
+      }
+      __syncwarp();
+      if (v && (31 - __clz(peers)) == lane) hist[w * 256 + d] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    uint64_t* t = a; a = b; b = t;
+  }
+  return a;
+}
+
+// ------------------------------------------------------------------ sweep
+// Union counts of tagged subsets over the sorted elements.  Each warp owns a
+// contiguous chunk; pass 1 finds per-warp maxima of the (masked, rescaled)
+// interval ends, pass 2 walks again with the carried running maximum.
+__device__ void sweep(const uint64_t* e, int64_t n, UnitSh& U, int64_t* wmax /* kMaxSub*kNW */) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t chunk = (((n + kNW - 1) / kNW) + 31) & ~int64_t(31);
+  const int64_t beg = min(n, (int64_t)w * chunk), end = min(n, beg + chunk);
+  const int ns = U.n_sub;
+  for (int s0 = 0; s0 < ns; s0 += 8) {
+    const int sn = min(8, ns - s0);
+    int64_t mx[8];
+    for (int q = 0; q < 8; ++q) mx[q] = -1;
+    for (int64_t i = beg + lane; i < end; i += 32) {
+      const uint64_t x = e[i];
+      const uint32_t tag = (uint32_t)(x & 31u);
+      const int64_t lo = (int64_t)(x >> kKeyShift);
+      const int64_t hi = lo + (int64_t)((x >> kTagBits) & kLenMask);
+      for (int q = 0; q < sn; ++q)
+        if ((U.sub_mask[s0 + q] >> tag) & 1u) mx[q] = max(mx[q], hi / U.sub_r[s0 + q]);
+    }
+    for (int q = 0; q < sn; ++q) {
+      int64_t v = mx[q];
+      for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (lane == 0) wmax[(s0 + q) * kNW + w] = v;
+    }
+    __syncthreads();
+    int64_t carry[8], cnt[8];
+    for (int q = 0; q < sn; ++q) {
+      int64_t r = -1;
+      for (int k = 0; k < w; ++k) r = max(r, wmax[(s0 + q) * kNW + k]);
+      carry[q] = r;
+      cnt[q] = 0;
+    }
+    for (int64_t i0 = beg; i0 < end; i0 += 32) {
+      const int64_t i = i0 + lane;
+      const bool v = i < end;
+      const uint64_t x = v ? e[i] : 0;
+      const uint32_t tag = (uint32_t)(x & 31u);
+      const int64_t lo0 = (int64_t)(x >> kKeyShift);
+      const int64_t hi0 = lo0 + (int64_t)((x >> kTagBits) & kLenMask);
+      for (int q = 0; q < sn; ++q) {
+        const bool in = v && ((U.sub_mask[s0 + q] >> tag) & 1u);
+        const int64_t r = U.sub_r[s0 + q];
+        const int64_t lo = in ? lo0 / r : -1, hi = in ? hi0 / r : -1;
+        // inclusive max-scan of hi across lanes
+        int64_t inc = hi;
+        for (int o = 1; o < 32; o <<= 1) {
+          int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc = max(inc, t);
+        }
+        int64_t before = __shfl_up_sync(0xffffffffu, inc, 1);
+        if (lane == 0) before = -1;
+        before = max(before, carry[q]);
+        if (in) {
+          if (lo > before) cnt[q] += hi - lo + 1;
+          else if (hi > before) cnt[q] += hi - before;
+        }
+        carry[q] = max(carry[q], __shfl_sync(0xffffffffu, inc, 31));
+      }
+    }
+    __syncthreads();
+    for (int q = 0; q < sn; ++q) {
+      int64_t v = cnt[q];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) wmax[(s0 + q) * kNW + w] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < sn) {
+      int64_t s = 0;
+      for (int k = 0; k < kNW; ++k) s += wmax[(s0 + threadIdx.x) * kNW + k];
+      U.sub_val[s0 + threadIdx.x] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ kernel
+struct SetsArgs {
+  TplView T;
+  const gvo_machine* machines;
+  const gvo_config* cfgs;
+  const Geo* geos;
+  const int64_t* coefs;
+  int64_t n_items;
+  int S_req;
+  int F_stride;
+  int mode;                 // 0 standard, 1 custom wave sets, 2 custom footprint
+  int64_t granularity;      // modes 1/2
+  const int64_t* run_start; // mode 2 runs
+  const int64_t* run_count;
+  int n_custom_runs;
+  int64_t* counts;          // mode 0: counts rows; modes 1/2: output
+  int64_t counts_stride;
+  uint8_t* slab;            // per-CTA scratch
+  int64_t slab_bytes;
+  int64_t run_cap;
+  int64_t elem_cap;
+  int* status_out;          // modes 1/2: unit status
+};
+
+__global__ void __launch_bounds__(kNT) k_sets(SetsArgs P) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  UnitSh& U = *reinterpret_cast<UnitSh*>(smem);
+  size_t off = (sizeof(UnitSh) + 15) & ~size_t(15);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + off); off += kNW * 256 * 4;
+  uint32_t* tot = reinterpret_cast<uint32_t*>(smem + off); off += 256 * 4;
+  int64_t* wmax = reinterpret_cast<int64_t*>(smem + off); off += kMaxSub * kNW * 8;
+  int64_t* roff_sh = reinterpret_cast<int64_t*>(smem + off); off += (kSmemRuns + 1) * 8;
+  uint64_t* ebuf = reinterpret_cast<uint64_t*>(smem + off);
+  const int64_t sm_elems = (int64_t)(kSetsSmemBytes - off) / 16;
+
+  uint8_t* slab = P.slab + (int64_t)blockIdx.x * P.slab_bytes;
+  Run* runs = reinterpret_cast<Run*>(slab);
+  int64_t* roff_gl = reinterpret_cast<int64_t*>(slab + P.run_cap * sizeof(Run));
+  uint64_t* gbuf = reinterpret_cast<uint64_t*>(slab + P.run_cap * sizeof(Run) + (P.run_cap + 1) * 8);
+
+  for (int64_t item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+    // ---------------- unit description
+    if (threadIdx.x == 0) {
+      U.status = GVO_OK;
+      U.n_runs = 0;
+      U.key_lo = INT64_MAX;
+      U.key_hi = INT64_MIN;
+      U.n_src = 0;
+      U.n_sub = 0;
+      int64_t c, f;
+      int j = 0;
+      bool skip = false;
+      if (P.mode == 0) {
+        const int64_t per_cfg = (int64_t)P.F_stride * (P.S_req + 1);
+        c = item / per_cfg;
+        f = (item % per_cfg) / (P.S_req + 1);
+        j = (int)(item % (P.S_req + 1));
+      } else {
+        c = 0;
+        f = item;
+      }
+      const Geo& G = P.geos[c];
+      const gvo_config& cfg = P.cfgs[c];
+      if (f >= P.T.n_fields[cfg.template_id]) skip = true;
+      if (P.mode == 0 && !phase_ok(G, j < P.S_req ? 0 : 1)) skip = true;
+      U.cfg = c;
+      U.field = (int)f;
+      U.j = j;
+      if (!skip && P.mode == 0 && j < P.S_req) {
+        if (j >= G.n_samples) skip = true;
+        else {
+          U.kind = 0;
+          U.n_src = 2;
+          for (int k = 0; k < 2; ++k) {
+            U.src_start[k] = G.sample_lin[j];
+            U.src_count[k] = 1;
+            U.src_kind[k] = k;
+            U.src_tag[k] = k;
+          }
+          U.n_sub = 3;
+          U.sub_mask[0] = 1; U.sub_r[0] = 1;            // load sectors
+          U.sub_mask[1] = 1; U.sub_r[1] = 1;            // load lines (r set below)
+          U.sub_mask[2] = 2; U.sub_r[2] = 1;            // store sectors
+        }
+      } else if (!skip && P.mode != 2) {
+        U.kind = 1;
+        U.n_src = 2 * G.n_uw;
+        for (int u = 0; u < G.n_uw; ++u)
+          for (int k = 0; k < 2; ++k) {
+            U.src_start[2 * u + k] = G.uw_start[u];
+            U.src_count[2 * u + k] = G.uw_count[u];
+            U.src_kind[2 * u + k] = k;
+            U.src_tag[2 * u + k] = 2 * u + k;
+          }
+        int q = 0;
+        for (int u = 0; u < G.n_uw; ++u) {
+          U.sub_mask[q] = 1u << (2 * u); U.sub_r[q++] = 1;
+          U.sub_mask[q] = 1u << (2 * u + 1); U.sub_r[q++] = 1;
+          U.sub_mask[q] = 3u << (2 * u); U.sub_r[q++] = 1;
+          U.sub_mask[q] = u ? (1u << (2 * u)) | (1u << (2 * u - 2)) : 0u; U.sub_r[q++] = 1;
+        }
+        U.n_sub = q;
+      } else if (!skip) {
+        U.kind = 2;
+        U.n_src = 0;
+        if (2 * P.n_custom_runs > kMaxSrc) { skip = true; atomicExch(P.status_out, GVO_ERR_UNSUPPORTED); }
+        for (int r = 0; r < P.n_custom_runs && U.n_src + 2 <= kMaxSrc; ++r)
+          for (int k = 0; k < 2; ++k) {
+            U.src_start[U.n_src] = P.run_start[r];
+            U.src_count[U.n_src] = P.run_count[r];
+            U.src_kind[U.n_src] = k;
+            U.src_tag[U.n_src] = k;
+            ++U.n_src;
+          }
+        U.n_sub = 2;
+        U.sub_mask[0] = 1; U.sub_r[0] = 1;
+        U.sub_mask[1] = 2; U.sub_r[1] = 1;
+      }
+      if (skip) U.n_src = -1;
+    }
+    __syncthreads();
+    if (U.n_src < 0) { __syncthreads(); continue; }
+
+    const int64_t c = U.cfg;
+    const Geo& G = P.geos[c];
+    const gvo_config cfg = P.cfgs[c];
+    const int tpl = cfg.template_id;
+    const int abase = P.T.acc_base[tpl];
+    const int64_t* fbase = P.T.field_base + P.T.field_base_off[tpl];
+    const int32_t bd[3] = {cfg.block[0], cfg.block[1], cfg.block[2]};
+    const int64_t gd[3] = {cfg.grid[0], cfg.grid[1], cfg.grid[2]};
+    const int64_t* crow = P.coefs + c * (int64_t)P.T.max_acc * 8;
+    const gvo_machine& mach = P.machines[cfg.machine_id];
+    const int64_t g = P.mode == 0 ? mach.sector_bytes : P.granularity;
+    const Granule Gr = Granule::make(g);
+    const int64_t R = P.mode == 0 ? mach.l1_line_bytes / mach.sector_bytes : 1;
+    if (threadIdx.x == 0) {
+      U.g = g;
+      U.R = R;
+      if (U.kind == 0) U.sub_r[1] = R;
+    }
+    const int64_t tpb = G.tpb;
+    RunSink sink{runs, (int)P.run_cap, &U.n_runs, &U.status, &U.key_lo, &U.key_hi};
+    __syncthreads();
+
+    // ---------------- run building: one thread per (source, box)
+    for (int task = threadIdx.x; task < U.n_src * 5; task += kNT) {
+      const int s = task / 5, bi = task % 5;
+      Box boxes[5];
+      const int nb = run_boxes(U.src_start[s], U.src_count[s], gd, boxes);
+      const int fk = P.T.fk_off[tpl * (2 * kMaxFields + 1) + U.field * 2 + U.src_kind[s]];
+      const int fk_end = P.T.fk_off[tpl * (2 * kMaxFields + 1) + U.field * 2 + U.src_kind[s] + 1];
+      const int na = fk_end - fk;
+      if (bi == 0) {  // points runs for non-affine accesses (whole source)
+        for (int q = 0; q < na; ++q) {
+          const int a = P.T.fk_list[fk + q];
+          if (crow[a * 8 + 7] == kAffine) continue;
+          int64_t clo[6], chi[6];
+          clo[0] = clo[1] = clo[2] = 0;
+          chi[0] = bd[0] - 1; chi[1] = bd[1] - 1; chi[2] = bd[2] - 1;
+          run_bid_bounds(U.src_start[s], U.src_count[s], gd, clo + 3, chi + 3);
+          int64_t lo, hi;
+          const int ga = abase + a;
+          bounds_check(P.T.code + P.T.code_off[ga], P.T.code_len[ga], clo, chi, bd, fbase, &lo, &hi);
+          const int slot = atomicAdd(&U.n_runs, 1);
+          if (slot >= P.run_cap) { atomicExch(&U.status, GVO_ERR_CAPACITY); continue; }
+          Run r;
+          r.kind = 1;
+          r.access = a;
+          r.tag = U.src_tag[s];
+          r.run_start = U.src_start[s];
+          r.run_count = U.src_count[s];
+          r.count = U.src_count[s] * tpb;
+          r.pieces = 1;
+          r.nd = 0;
+          r.base = 0;
+          r.span = 0;
+          runs[slot] = r;
+          atomicMin((long long*)&U.key_lo, (long long)Gr.of(lo));
+          atomicMax((long long*)&U.key_hi, (long long)Gr.of(hi));
+        }
+      }
+      if (bi >= nb) continue;
+      const Box box = boxes[bi];
+      // coefficient classes (accesses with identical thread/block coefficients)
+      uint32_t done[GVO_MAX_ACCESSES / 32];
+      for (int q = 0; q < (na + 31) / 32; ++q) done[q] = 0;
+      for (int q = 0; q < na; ++q) {
+        const int a = P.T.fk_list[fk + q];
+        if (crow[a * 8 + 7] != kAffine) continue;
+        if ((done[q >> 5] >> (q & 31)) & 1u) continue;
+        const int64_t* ca = crow + a * 8;
+        const Lat L0 = box_lattice(ca, bd, box, Gr);
+        int64_t pts[kClassPts];
+        int np = 0;
+        for (int q2 = q; q2 < na; ++q2) {
+          if ((done[q2 >> 5] >> (q2 & 31)) & 1u) continue;
+          const int a2 = P.T.fk_list[fk + q2];
+          const int64_t* cb = crow + a2 * 8;
+          if (cb[7] != kAffine) continue;
+          bool same = true;
+          for (int k = 1; k < 7; ++k) same &= cb[k] == ca[k];
+          if (!same) continue;
+          done[q2 >> 5] |= 1u << (q2 & 31);
+          // translate of L0 by the access constant
+          const int64_t p = (int64_t)((uint64_t)L0.base + (uint64_t)cb[0]);
+          // insertion into sorted unique list
+          int k = np;
+          bool dup = false;
+          while (k > 0 && pts[k - 1] >= p) { if (pts[k - 1] == p) { dup = true; break; } --k; }
+          if (dup) continue;
+          for (int m = np; m > k; --m) pts[m] = pts[m - 1];
+          pts[k] = p;
+          ++np;
+          if (np == kClassPts) { cover_and_emit(sink, L0, pts, np, U.src_tag[s], Gr); np = 0; }
+        }
+        if (np) cover_and_emit(sink, L0, pts, np, U.src_tag[s], Gr);
+      }
+    }
+    __syncthreads();
+
+    // ---------------- offsets of runs, element count
+    const int nr = min(U.n_runs, (int)P.run_cap);
+    int64_t* roff = nr <= kSmemRuns ? roff_sh : roff_gl;
+    if (threadIdx.x == 0) {
+      int64_t acc = 0;
+      for (int r = 0; r < nr; ++r) { roff[r] = acc; acc += runs[r].count; }
+      roff[nr] = acc;
+      U.N = acc;
+      const int64_t base = floordiv(U.key_lo, U.R) * U.R;
+      U.key_lo = base;
+      if (U.status == GVO_OK) {
+        if (nr > 0 && (uint64_t)(U.key_hi - base) >= (uint64_t(1) << kKeyBits)) U.status = GVO_ERR_UNSUPPORTED;
+        if (acc > P.elem_cap) U.status = GVO_ERR_CAPACITY;
+      }
+    }
+    __syncthreads();
+    if (U.status != GVO_OK) {
+      if (threadIdx.x == 0) {
+        if (P.mode == 0) {
+          int64_t* row = P.counts + c * P.counts_stride;
+          atomicExch((unsigned long long*)&row[GVO_C_STATUS], (unsigned long long)U.status);
+        } else {
+          atomicExch(P.status_out, U.status);
+        }
+      }
+      __syncthreads();
+      continue;
+    }
+    const int64_t N = U.N;
+    uint64_t* A0;
+    uint64_t* B0;
+    if (N <= sm_elems) { A0 = ebuf; B0 = ebuf + sm_elems; }
+    else { A0 = gbuf; B0 = gbuf + P.elem_cap; }
+    const int64_t kbase = U.key_lo;
+
+    // ---------------- emission
+    for (int64_t i = threadIdx.x; i < N; i += kNT) {
+      int lo = 0, hi = nr - 1;
+      while (lo < hi) {  // last run with roff[r] <= i
+        int mid = (lo + hi + 1) >> 1;
+        if (roff[mid] <= i) lo = mid; else hi = mid - 1;
+      }
+      const Run& r = runs[lo];
+      int64_t k = i - roff[lo];
+      int64_t glo, ghi;
+      if (r.kind == 0) {
+        const int64_t piece = k % r.pieces;
+        k /= r.pieces;
+        uint64_t b = (uint64_t)r.base;
+        for (int d = r.nd - 1; d >= 0; --d) {
+          const int64_t idx = k % r.ext[d];
+          k /= r.ext[d];
+          b += (uint64_t)r.stride[d] * (uint64_t)idx;
+        }
+        glo = Gr.of((int64_t)b);
+        ghi = Gr.of((int64_t)(b + r.span));
+        if (r.pieces > 1) {
+          int64_t plo = glo + piece * kPiece;
+          if (plo > ghi) plo = glo;
+          const int64_t phi = min(ghi, plo + kPiece - 1);
+          glo = plo;
+          ghi = phi;
+        }
+      } else {
+        const int64_t blk = r.run_start + k / tpb;
+        const int64_t th = k % tpb;
+        int64_t crd[6];
+        crd[0] = th % bd[0];
+        crd[1] = (th / bd[0]) % bd[1];
+        crd[2] = th / ((int64_t)bd[0] * bd[1]);
+        crd[3] = blk % gd[0];
+        crd[4] = (blk / gd[0]) % gd[1];
+        crd[5] = blk / (gd[0] * gd[1]);
+        const int ga = abase + r.access;
+        glo = ghi = Gr.of(eval_point(P.T.code + P.T.code_off[ga], P.T.code_len[ga], crd, bd, fbase));
+      }
+      A0[i] = ((uint64_t)(glo - kbase) << kKeyShift) | ((uint64_t)(ghi - glo) << kTagBits) |
+              (uint64_t)r.tag;
+    }
+    __syncthreads();
+
+    // ---------------- sort + sweeps
+    int kb = 0;
+    {
+      uint64_t span = (uint64_t)(U.key_hi - kbase);
+      while (span) { ++kb; span >>= 1; }
+    }
+    const int nbits = ((kb + 7) / 8) * 8;
+    const uint64_t* sorted = cta_sort(A0, B0, N, kKeyShift, nbits, hist, tot);
+    sweep(sorted, N, U, wmax);
+
+    // ---------------- outputs
+    if (threadIdx.x == 0) {
+      const int f = U.field;
+      if (P.mode == 0) {
+        int64_t* row = P.counts + c * P.counts_stride;
+        if (U.kind == 0) {
+          int64_t* b = row + GVO_C_HDR + ((int64_t)U.j * P.F_stride + f) * 5;
+          b[0] = U.sub_val[0];
+          b[2] = U.sub_val[1];
+          b[3] = U.sub_val[2];
+        } else {
+          int64_t* wv = row + GVO_C_HDR + (int64_t)P.S_req * P.F_stride * 5;
+          for (int u = 0; u < G.n_uw; ++u) {
+            int64_t* o = wv + ((int64_t)u * P.F_stride + f) * 4;
+            o[0] = U.sub_val[4 * u + 0];
+            o[1] = U.sub_val[4 * u + 1];
+            o[2] = U.sub_val[4 * u + 2];
+            o[3] = u ? U.sub_val[4 * u] + U.sub_val[4 * (u - 1)] - U.sub_val[4 * u + 3] : 0;
+          }
+        }
+      } else if (P.mode == 1) {
+        for (int u = 0; u < G.n_uw; ++u) {
+          int64_t* o = P.counts + ((int64_t)u * P.F_stride + f) * 4;
+          o[0] = U.sub_val[4 * u + 0];
+          o[1] = U.sub_val[4 * u + 1];
+          o[2] = U.sub_val[4 * u + 2];
+          o[3] = u ? U.sub_val[4 * u] + U.sub_val[4 * (u - 1)] - U.sub_val[4 * u + 3] : 0;
+        }
+      } else {
+        P.counts[f * 2 + 0] = U.sub_val[0];
+        P.counts[f * 2 + 1] = U.sub_val[1];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+void launch_sets(const SetsLaunch& L, cudaStream_t st) {
+  SetsArgs P;
+  P.T = L.T;
+  P.machines = L.machines;
+  P.cfgs = L.cfgs;
+  P.geos = L.geos;
+  P.coefs = L.coefs;
+  P.n_items = L.n_items;
+  P.S_req = L.S_req;
+  P.F_stride = L.F_stride;
+  P.mode = L.mode;
+  P.granularity = L.granularity;
+  P.run_start = L.run_start;
+  P.run_count = L.run_count;
+  P.n_custom_runs = L.n_custom_runs;
+  P.counts = L.counts;
+  P.counts_stride = L.counts_stride;
+  P.slab = L.slab;
+  P.slab_bytes = L.slab_bytes;
+  P.run_cap = L.run_cap;
+  P.elem_cap = L.elem_cap;
+  P.status_out = L.status_out;
+  if (P.n_items <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sets, cudaFuncAttributeMaxDynamicSharedMemorySize, kSetsSmemBytes);
+    attr = true;
+  }
+  const int64_t grid = P.n_items < L.n_ctas ? P.n_items : L.n_ctas;
+  k_sets<<<(unsigned)grid, kNT, kSetsSmemBytes, st>>>(P);
+}
+
+int64_t sets_slab_bytes(int64_t run_cap, int64_t elem_cap) {
+  return ((run_cap * (int64_t)sizeof(Run) + (run_cap + 1) * 8 + 2 * elem_cap * 8) + 255) & ~int64_t(255);
+}
+
+}  // namespace gvo

@@ -1,0 +1,191 @@
+"""Device parity: the sm_100a engine vs the reference golden vectors and the
+CPU oracle.  Integer volumes bit-exact, floats bit-exact (tolerance 0 —
+stricter than north_star's 1e-6 relative), rankings identical."""
+
+import math
+
+import numpy as np
+import pytest
+
+from golden_util import load, unhex
+from oracle import gvo_oracle as ora
+from paper_2107_01143_b200 import gvo
+from paper_2107_01143_b200.gvo.footprint import CollaborativeGroup, wave_footprint
+from paper_2107_01143_b200.gvo.machine import machine_from_dict
+
+pytestmark = pytest.mark.gpu
+
+
+def test_native_library_loaded():
+    from paper_2107_01143_b200 import _native
+
+    ctx = _native.context()
+    assert ctx.h
+
+
+def test_footprints_match_reference_golden():
+    bad = []
+    for case in load("footprints"):
+        k = gvo.kernel_from_dict(case["spec"])
+        grp = CollaborativeGroup(k.launch, np.asarray(case["blocks"], dtype=np.int64), "L2")
+        r = gvo.grid_iteration(k, grp, case["granularity"])
+        got = {(f, kd): (c.unique_count, c.total_count) for (f, kd), c in r.per_field.items()}
+        want = {(f, kd): (u, t) for f, kd, u, t in case["per_field"]}
+        if got != want:
+            bad.append((case["spec"]["accesses"], case["blocks"], case["granularity"], got, want))
+    assert not bad, bad[:3]
+
+
+def _compare_eval(case):
+    k = gvo.kernel_from_dict(case["spec"])
+    m = machine_from_dict(case["machine"])
+    bsz, wsz, ovr = case["sampling"]
+    p = gvo.evaluate_kernel(k, m, block_samples=bsz, wave_samples=wsz, override_blocks_per_wave=ovr)
+    v = p.volumes
+    got = {
+        "l1CyclesPerLup": p.l1_cycles.cycles_per_lup,
+        "l2l1LoadComp": v.l2l1_load.v_comp, "l2l1LoadRed": v.l2l1_load.v_red, "l2l1LoadCap": v.l2l1_load.v_cap,
+        "l2l1LoadUp": v.l2l1_load.v_up, "l2l1LoadDown": v.l2l1_load.v_down, "l2l1LoadAlloc": v.l2l1_load.v_alloc,
+        "l2l1LoadOversub": v.l2l1_load.oversubscription,
+        "l2l1StoreComp": v.l2l1_store.v_comp, "l2l1StoreRed": v.l2l1_store.v_red,
+        "l2l1StoreCap": v.l2l1_store.v_cap, "l2l1StoreUp": v.l2l1_store.v_up, "l2l1StoreDown": v.l2l1_store.v_down,
+        "dramLoadComp": v.dram_load.v_comp, "dramLoadRed": v.dram_load.v_red, "dramLoadCap": v.dram_load.v_cap,
+        "dramLoadUp": v.dram_load.v_up, "dramLoadDown": v.dram_load.v_down, "dramLoadAlloc": v.dram_load.v_alloc,
+        "dramLoadOversub": v.dram_load.oversubscription, "dramLoadUnique": v.dram_load.wave_unique,
+        "dramLoadOverlap": v.dram_load.v_overlap, "dramLoadOvermiss": v.dram_load.overmiss_bytes,
+        "dramLoadCoverage": v.dram_load.coverage, "dramLoadRedL2": v.dram_load.v_red_l2,
+        "dramStoreComp": v.dram_store.v_comp, "dramStoreRed": v.dram_store.v_red, "dramStoreCap": v.dram_store.v_cap,
+        "dramStoreUp": v.dram_store.v_up, "dramStoreDown": v.dram_store.v_down,
+        "dramStoreUnique": v.dram_store.wave_unique,
+        "tDram": p.times["dram"], "tL2": p.times["l2"], "tL1": p.times["l1"], "tFp": p.times["fp"],
+        "limiter": p.limiter, "predictedGLups": p.glups,
+    }
+    diffs = []
+    for col, want in case["record"].items():
+        if col in ("configKey", "blockX", "blockY", "blockZ", "folding"):
+            continue
+        w = unhex(want)
+        if got[col] != w:
+            diffs.append((col, got[col], w))
+    per = [float(x).hex() for x in p.l1_cycles.per_access]
+    if per != case["per_access"]:
+        diffs.append(("per_access", per[:4], case["per_access"][:4]))
+    for lvl, d in case["per_field_down"].items():
+        gv = getattr(v, lvl).per_field_down
+        for f, w in d.items():
+            if gv[f] != unhex(w):
+                diffs.append((lvl, f, gv[f], unhex(w)))
+    return diffs
+
+
+@pytest.mark.parametrize("idx", range(len(load("evaluations"))))
+def test_evaluate_kernel_bit_exact_vs_reference(idx):
+    case = load("evaluations")[idx]
+    diffs = _compare_eval(case)
+    assert not diffs, diffs
+
+
+def test_block_and_wave_integers_vs_reference():
+    for case in load("evaluations"):
+        if "block_ints" not in case:
+            continue
+        k = gvo.kernel_from_dict(case["spec"])
+        m = machine_from_dict(case["machine"])
+        for bi in case["block_ints"]:
+            grp = gvo.block_group(k.launch, bi["block"])
+            r32 = gvo.grid_iteration(k, grp, m.sector_bytes)
+            assert [[f, kd, c.unique_count, c.total_count] for (f, kd), c in r32.per_field.items()] == bi["sector"]
+            r128 = gvo.grid_iteration(k, grp, m.l1_line_bytes, kinds=("load",))
+            assert [[f, kd, c.unique_count, c.total_count] for (f, kd), c in r128.per_field.items()] == bi["line"]
+        waves = {}
+        for wi in case["wave_ints"]:
+            w = gvo.Wave(wi["index"], wi["start"], wi["count"])
+            fp = wave_footprint(k, w, m.sector_bytes)
+            waves[w.index] = (w, fp)
+            assert {f: s.count for f, s in fp.load_sets.items()} == wi["load"]
+            assert fp.store_counts == wi["store"]
+            assert fp.alloc_count == wi["alloc"]
+        for ov in case["overlaps"]:
+            (wc, fc), (wp, fpv) = waves[ov["curr"]], waves[ov["prev"]]
+            got = {f: fc.load_sets[f].intersection_count(fpv.load_sets[f]) for f in fc.load_sets}
+            assert got == ov["per_field"]
+
+
+def test_block_and_wave_stats_bit_exact():
+    for case in load("evaluations")[:6]:
+        k = gvo.kernel_from_dict(case["spec"])
+        m = machine_from_dict(case["machine"])
+        bsz, wsz, ovr = case["sampling"]
+        bs = gvo.sample_block_stats(k, m, bsz)
+        for key, d in case["block_stats"].items():
+            assert {f: float(v).hex() for f, v in getattr(bs, key).items()} == d, key
+        ws = gvo.sample_wave_stats(k, m, wsz, ovr)
+        for key in ("load_unique", "load_overlap", "store_unique"):
+            assert {f: float(v).hex() for f, v in getattr(ws, key).items()} == case["wave_stats"][key]
+        for key in ("prev_unique_total", "alloc_total", "wave_lups"):
+            assert float(getattr(ws, key)).hex() == case["wave_stats"][key]
+        assert ws.has_predecessor == case["wave_stats"]["has_predecessor"]
+
+
+def test_rank_sweep_order_identical_to_reference():
+    for sw in load("sweeps"):
+        fam = gvo.KernelFamily(sw["kind"], tuple(sw["grid"]), radius=sw["radius"])
+        cfgs = gvo.enumerate_sweep(sw["threads"], foldings=sw["foldings"])
+        rows = gvo.rank_sweep(fam, cfgs, gvo.v100_preset(), wave_samples=1, block_samples=2, skip_invalid=True)
+        assert [r.config.key for r in rows] == sw["order"]
+        assert [float(r.prediction.glups).hex() for r in rows] == sw["glups"]
+
+
+def _rand_kernel(rng, divmod_ok):
+    coords = ("tidx", "tidy", "tidz", "bidx", "bidy", "bidz")
+    block = [(1, 1, 1), (4, 1, 1), (8, 2, 1), (16, 2, 2), (32, 2, 1), (7, 3, 2), (33, 1, 2), (64, 2, 1)][rng.integers(0, 8)]
+    grid = [(1, 1, 1), (2, 1, 1), (2, 2, 1), (3, 2, 2), (5, 3, 2)][rng.integers(0, 5)]
+    names = [f"f{i}" for i in range(int(rng.integers(1, 4)))]
+    fields = tuple(gvo.Field(n, 8, (1 << 20,), alignment=int(rng.choice([0, -1, 8, 100]))) for n in names)
+    acc = []
+    for _ in range(int(rng.integers(1, 7))):
+        n = names[rng.integers(0, len(names))]
+        terms = " + ".join(f"{coords[rng.integers(0, 6)]} * {int(rng.integers(-64, 65))}"
+                           for _ in range(int(rng.integers(0, 5)))) or "0"
+        text = f"{n} + ({terms}) + {int(rng.integers(-256, 257))}"
+        if divmod_ok and rng.integers(0, 2):
+            text = f"{n} + (({terms}) {['//', '%'][rng.integers(0, 2)]} {int(rng.choice([2, 4, 32, 100]))})"
+        acc.append(gvo.Access(n, ["load", "store"][rng.integers(0, 2)], gvo.parse(text, fields=names),
+                              int(rng.integers(1, 4))))
+    return gvo.KernelDescriptor(fields=fields, accesses=tuple(acc), launch=gvo.LaunchConfig(block, grid))
+
+
+def test_random_kernels_vs_oracle():
+    rng = np.random.default_rng(7)
+    for i in range(300):
+        k = _rand_kernel(rng, divmod_ok=i % 2 == 0)
+        nb = k.launch.total_blocks
+        cnt = int(rng.integers(1, nb + 1))
+        start = int(rng.integers(0, nb - cnt + 1))
+        g = int(rng.choice([1, 8, 24, 32, 128]))
+        grp = CollaborativeGroup(k.launch, np.arange(start, start + cnt, dtype=np.int64), "L2")
+        r = gvo.grid_iteration(k, grp, g)
+        got = {(f, kd): (c.unique_count, c.total_count) for (f, kd), c in r.per_field.items()}
+        assert got == ora.footprint(k, grp.block_linear, g), (i, [gvo.render(a.expr) for a in k.accesses])
+
+
+def test_random_kernels_l1_cycles_vs_oracle():
+    rng = np.random.default_rng(11)
+    m = gvo.v100_preset()
+    for i in range(120):
+        k = _rand_kernel(rng, divmod_ok=i % 3 == 0)
+        b = int(rng.integers(0, k.launch.total_blocks))
+        est = gvo.volumes.l1_register_cycles(k, m, gvo.block_group(k.launch, b))
+        cyc, per = ora.l1_cycles(k, m, b)
+        assert est.cycles_per_lup == cyc and est.per_access == per, i
+
+
+def test_lbm_and_layout_variants_vs_oracle():
+    m = gvo.b200_preset()
+    cases = [gvo.generate_lbm_d3q15((64, 32, 32), (16, 2, 2)), gvo.generate_lbm_d3q15((64, 32, 32), (1, 8, 4)),
+             gvo.generate_star_stencil(3, (64, 64, 64), (8, 8, 2), "2z")]
+    for k in cases:
+        p = gvo.evaluate_kernel(k, m)
+        ev = ora.evaluate_kernel(k, m)
+        assert p.glups == ev["glups"] and p.limiter == ev["limiter"]
+        assert p.volumes.dram_load.v_down == ev["volumes"]["dram_load"]["down"]
