@@ -297,6 +297,10 @@ int gvo_set_timing(gvo_ctx* ctx, int enable);
 /* Accumulated ms / launch counts per kernel: [0] setup, [1] warp stats,
  * [2] interval-union sets, [3] assembly, [4] rank; 8 slots. */
 int gvo_kernel_times(gvo_ctx* ctx, double* ms_out, int64_t* count_out, int reset);
+/* Profiling: enable per-unit statistics of the interval-union engine and
+ * fetch those of the last batch: [item][runs, intervals, in-smem, cycles,
+ * key bits, SM id]; items ordered (config, field, unit). */
+int gvo_debug_units(gvo_ctx* ctx, int enable, int64_t* h_out, int64_t cap, int64_t* n_items);
 /* Measured INT32 issue rate of the device (ops/s), the integer roofline. */
 int gvo_int_peak(gvo_ctx* ctx, double* ops_per_s);
 

@@ -149,6 +149,7 @@ def lib():
             "gvo_set_timing": (C.c_int, [P, C.c_int]),
             "gvo_kernel_times": (C.c_int, [P, P, P, C.c_int]),
             "gvo_int_peak": (C.c_int, [P, C.POINTER(C.c_double)]),
+            "gvo_debug_units": (C.c_int, [P, C.c_int, P, i64, C.POINTER(C.c_int64)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -165,6 +166,7 @@ EXPORTED_SYMBOLS = (
     "gvo_set_machines", "gvo_counts_stride_eff", "gvo_eval_configs", "gvo_eval_configs_host",
     "gvo_rank", "gvo_group_footprint", "gvo_group_sets", "gvo_l1_cycles", "gvo_eval_addresses",
     "gvo_assemble_host", "gvo_predict_host", "gvo_set_timing", "gvo_kernel_times", "gvo_int_peak",
+    "gvo_debug_units",
 )
 
 

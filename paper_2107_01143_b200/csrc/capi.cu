@@ -83,11 +83,13 @@ struct gvo_ctx {
   DBuf<gvo_machine> d_machines;
   // work
   DBuf<int64_t> coefs;
+  DBuf<int64_t> ctabs;
   DBuf<Geo> geos;
   DBuf<uint8_t> slab;
   int64_t run_cap = 4096, elem_cap = 1 << 19, slab_bytes = 0;
   int n_ctas = 0;
   DBuf<int> status;
+  DBuf<unsigned long long> work;
   DBuf<uint8_t> rank_scratch;
   // host-variant staging
   DBuf<gvo_config> s_cfgs;
@@ -101,6 +103,10 @@ struct gvo_ctx {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
   double kernel_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int64_t kernel_launches[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  // optional per-unit statistics of the set engine (profiling)
+  bool unit_debug = false;
+  DBuf<int64_t> unit_stats;
+  int64_t unit_items = 0;
 };
 
 // kernel ids for timing: 0 setup, 1 warp, 2 sets, 3 finish, 4 rank
@@ -293,12 +299,13 @@ int gvo_set_machines(gvo_ctx* ctx, const gvo_machine* m, int32_t n) {
 static int ensure_work(gvo_ctx* ctx, int64_t n) {
   if (!ctx->coefs.ensure((size_t)n * ctx->max_acc * 8)) return set_err(ctx, GVO_ERR_CUDA, "coefficient table alloc failed%s");
   if (!ctx->geos.ensure((size_t)n)) return set_err(ctx, GVO_ERR_CUDA, "geometry alloc failed%s");
+  if (!ctx->ctabs.ensure((size_t)n * ctab_stride(ctx->max_acc))) return set_err(ctx, GVO_ERR_CUDA, "class table alloc failed%s");
   if (ctx->slab_bytes == 0) {
     ctx->slab_bytes = sets_slab_bytes(ctx->run_cap, ctx->elem_cap);
     if (!ctx->slab.ensure((size_t)ctx->slab_bytes * ctx->n_ctas))
       return set_err(ctx, GVO_ERR_CUDA, "scratch slab alloc failed%s");
   }
-  if (!ctx->status.ensure(4)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
+  if (!ctx->status.ensure(4) || !ctx->work.ensure(1)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
   return GVO_OK;
 }
 
@@ -334,7 +341,7 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     CK(cudaMemsetAsync(cnt, 0, (size_t)nb * stride * 8, st));
     cudaEvent_t tb = nullptr;
     tmark_begin(ctx, 0, st, &tb);
-    launch_setup(ctx->view, ctx->d_machines.p, cf, nb, *sampling, ctx->coefs.p, ctx->geos.p, st);
+    launch_setup(ctx->view, ctx->d_machines.p, cf, nb, *sampling, ctx->coefs.p, ctx->geos.p, ctx->ctabs.p, st);
     tmark_end(ctx, 0, st, tb);
     tmark_begin(ctx, 1, st, &tb);
     launch_warp(ctx->view, ctx->d_machines.p, cf, ctx->geos.p, ctx->coefs.p, nb * (S + 1), S, m0.sector_bytes,
@@ -348,6 +355,7 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     L.cfgs = cf;
     L.geos = ctx->geos.p;
     L.coefs = ctx->coefs.p;
+    L.ctabs = ctx->ctabs.p;
     L.n_items = nb * F * (S + 1);
     L.S_req = S;
     L.F_stride = F;
@@ -360,6 +368,14 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     L.elem_cap = ctx->elem_cap;
     L.status_out = ctx->status.p;
     L.n_ctas = ctx->n_ctas;
+    L.work = ctx->work.p;
+  L.work = ctx->work.p;
+    if (ctx->unit_debug) {
+      if (!ctx->unit_stats.ensure((size_t)L.n_items * 10)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
+      CK(cudaMemsetAsync(ctx->unit_stats.p, 0, (size_t)L.n_items * 10 * 8, st));
+      L.unit_stats = ctx->unit_stats.p;
+      ctx->unit_items = L.n_items;
+    }
     tmark_begin(ctx, 2, st, &tb);
     launch_sets(L, st);
     tmark_end(ctx, 2, st, tb);
@@ -431,6 +447,7 @@ static int one_config(gvo_ctx* ctx, int32_t tpl, const int32_t block[3], const i
   if (!ctx->s_cfgs.ensure(1)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
   CK(cudaMemcpyAsync(ctx->s_cfgs.p, &c, sizeof c, cudaMemcpyHostToDevice, ctx->stream));
   k_coefs_only<<<1, 32, 0, ctx->stream>>>(ctx->view, ctx->s_cfgs.p, 1, ctx->coefs.p);
+  launch_classes(ctx->view, ctx->s_cfgs.p, 1, ctx->coefs.p, ctx->ctabs.p, ctx->stream);
   CK(cudaGetLastError());
   return GVO_OK;
 }
@@ -469,6 +486,7 @@ int gvo_group_footprint(gvo_ctx* ctx, int32_t tpl, const int32_t block[3], const
   L.cfgs = ctx->s_cfgs.p;
   L.geos = ctx->geos.p;
   L.coefs = ctx->coefs.p;
+  L.ctabs = ctx->ctabs.p;
   L.n_items = F;
   L.S_req = 0;
   L.F_stride = F;
@@ -485,6 +503,7 @@ int gvo_group_footprint(gvo_ctx* ctx, int32_t tpl, const int32_t block[3], const
   L.elem_cap = ctx->elem_cap;
   L.status_out = ctx->status.p;
   L.n_ctas = ctx->n_ctas;
+  L.work = ctx->work.p;
   launch_sets(L, st);
   launch_warp(ctx->view, ctx->d_machines.p, ctx->s_cfgs.p, ctx->geos.p, ctx->coefs.p, (int64_t)blocks.size(), 0, granularity, 1, 1, 1,
               ctx->s_i64c.p, nullptr, 0, F, nullptr, 0, ctx->s_ull.p, ctx->max_acc, ctx->n_sm, st);
@@ -533,6 +552,7 @@ int gvo_group_sets(gvo_ctx* ctx, int32_t tpl, const int32_t block[3], const int6
   L.cfgs = ctx->s_cfgs.p;
   L.geos = ctx->geos.p;
   L.coefs = ctx->coefs.p;
+  L.ctabs = ctx->ctabs.p;
   L.n_items = F;
   L.F_stride = F;
   L.mode = 1;
@@ -544,6 +564,7 @@ int gvo_group_sets(gvo_ctx* ctx, int32_t tpl, const int32_t block[3], const int6
   L.elem_cap = ctx->elem_cap;
   L.status_out = ctx->status.p;
   L.n_ctas = ctx->n_ctas;
+  L.work = ctx->work.p;
   launch_sets(L, st);
   CK(cudaGetLastError());
   int status = 0;
@@ -640,6 +661,17 @@ int gvo_kernel_times(gvo_ctx* ctx, double* ms_out, int64_t* count_out, int reset
     if (ms_out) ms_out[k] = ctx->kernel_ms[k];
     if (count_out) count_out[k] = ctx->kernel_launches[k];
     if (reset) { ctx->kernel_ms[k] = 0; ctx->kernel_launches[k] = 0; }
+  }
+  return GVO_OK;
+}
+
+int gvo_debug_units(gvo_ctx* ctx, int enable, int64_t* h_out, int64_t cap, int64_t* n_items) {
+  if (!ctx) return GVO_ERR_INVALID;
+  ctx->unit_debug = enable != 0;
+  if (n_items) *n_items = ctx->unit_items;
+  if (h_out && ctx->unit_items) {
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(h_out, ctx->unit_stats.p, std::min<int64_t>(cap, ctx->unit_items) * 10 * 8, cudaMemcpyDeviceToHost));
   }
   return GVO_OK;
 }

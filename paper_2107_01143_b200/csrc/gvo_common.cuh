@@ -79,6 +79,27 @@ struct TplView {
   int32_t max_acc;         // max accesses over templates (coef row stride)
 };
 
+// ---------------------------------------------------------------- classes
+// Per config "class table" (int64 words), written by k_setup.  Affine
+// accesses of one (field, kind) slot with identical thread/block
+// coefficients form a class: translates of one lattice by their constants.
+//   [0, 2F+1)          first class of each slot (F = kMaxFields)
+//   start[A], cnt[A]   class -> range of its sorted unique constants in pts
+//   rep[A]             class -> representative access
+//   pts[A]             constants, sorted ascending, unique per class
+//   rep_of[A]          access -> representative access (-1: non-affine)
+__host__ __device__ constexpr int64_t ctab_stride(int64_t A) { return 2 * kMaxFields + 1 + 5 * A; }
+struct CTab {
+  int64_t* base;
+  int64_t A;
+  __host__ __device__ int64_t* slot_first() const { return base; }
+  __host__ __device__ int64_t* start() const { return base + 2 * kMaxFields + 1; }
+  __host__ __device__ int64_t* cnt() const { return start() + A; }
+  __host__ __device__ int64_t* rep() const { return cnt() + A; }
+  __host__ __device__ int64_t* pts() const { return rep() + A; }
+  __host__ __device__ int64_t* rep_of() const { return pts() + A; }
+};
+
 // ---------------------------------------------------------------- geometry
 // Per-config plan written by the setup kernel.
 struct Geo {
@@ -95,6 +116,10 @@ struct Geo {
   int64_t sample_lin[kMaxSamples];
   int64_t uw_start[kMaxUWaves];
   int64_t uw_count[kMaxUWaves];
+  // block-sample dedup: dup_of[f][j] = earlier sample whose unique-granule
+  // sets of field f are exact translates of sample j's by a multiple of the
+  // line size (so every sector/line count is identical), or -1
+  int8_t dup_of[kMaxFields][kMaxSamples];
 };
 
 // A unit of phase p runs when the phase was requested and no error was

@@ -9,8 +9,10 @@ namespace gvo {
 constexpr int kSetsSmemBytes = 112 * 1024;
 
 void launch_setup(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs,
-                  int64_t n, const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos,
+                  int64_t n, const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos, int64_t* d_ctabs,
                   cudaStream_t st);
+void launch_classes(const TplView& T, const gvo_config* d_cfgs, int64_t n, const int64_t* d_coefs,
+                    int64_t* d_ctabs, cudaStream_t st);
 
 void launch_warp(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs, const Geo* d_geos, const int64_t* d_coefs,
                  int64_t n_items, int S_req, int64_t sector, int64_t bank_width, int64_t n_banks,
@@ -24,6 +26,7 @@ struct SetsLaunch {
   const gvo_config* cfgs;
   const Geo* geos;
   const int64_t* coefs;
+  const int64_t* ctabs;
   int64_t n_items;
   int S_req;
   int F_stride;
@@ -40,6 +43,8 @@ struct SetsLaunch {
   int64_t elem_cap;
   int* status_out;
   int n_ctas;
+  int64_t* unit_stats = nullptr;
+  unsigned long long* work = nullptr;
 };
 void launch_sets(const SetsLaunch& L, cudaStream_t st);
 int64_t sets_slab_bytes(int64_t run_cap, int64_t elem_cap);

@@ -265,6 +265,16 @@ __global__ void k_finish(TplView T, const gvo_machine* machines, const gvo_confi
   const double lups = (double)G.lups_per_block;
   // ---- BlockStats (volumes.py:152-185)
   for (int k = 0; k < 10 * Ft + 7; ++k) st[k] = 0.0;
+  // resolve deduplicated samples (unique counts copied from the
+  // translate-equivalent sample; warp counts were computed per sample)
+  for (int s = 0; ph0 && s < G.n_samples; ++s)
+    for (int f = 0; f < Ft; ++f) {
+      const int d = G.dup_of[f][s];
+      if (d < 0) continue;
+      int64_t* b = blk + ((int64_t)s * F + f) * 5;
+      const int64_t* o = blk + ((int64_t)d * F + f) * 5;
+      for (int k = 0; k < 5; ++k) b[k] = o[k];
+    }
   for (int s = 0; ph0 && s < G.n_samples; ++s)
     for (int f = 0; f < Ft; ++f) {
       const int64_t* b = blk + ((int64_t)s * F + f) * 5;

@@ -114,6 +114,33 @@ __global__ void k_tile_scatter(const uint64_t* key, const uint32_t* idx, int64_t
   }
 }
 
+// Small batches: one CTA computes each element's rank by counting the
+// elements ordered before it (lexicographic (k1, k2, index) => stable), one
+// launch instead of 51.
+constexpr int kSmallRank = 2048;
+__global__ void __launch_bounds__(1024) k_rank_small(const double* rec, const gvo_config* cfgs, int64_t n,
+                                                     int64_t* order) {
+  __shared__ uint64_t s1[kSmallRank], s2[kSmallRank];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    uint64_t b = (uint64_t)__double_as_longlong(rec[i * GVO_RECORD_LEN + GVO_R_GLUPS]);
+    b = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    s1[i] = ~b;
+    const gvo_config c = cfgs[i];
+    s2[i] = ((uint64_t)(c.block[0] & 0xfffff) << 42) | ((uint64_t)(c.block[1] & 0xfffff) << 22) |
+            ((uint64_t)(c.block[2] & 0xfffff) << 2) | (uint64_t)(c.fold_rank & 3);
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t a1 = s1[i], a2 = s2[i];
+    int64_t r = 0;
+    for (int64_t j = 0; j < n; ++j) {
+      const uint64_t b1 = s1[j], b2 = s2[j];
+      r += (b1 < a1) || (b1 == a1 && (b2 < a2 || (b2 == a2 && j < i)));
+    }
+    order[r] = i;
+  }
+}
+
 __global__ void k_order_out(const uint32_t* idx, int64_t n, int64_t* order) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) order[i] = idx[i];
@@ -127,6 +154,10 @@ int64_t rank_scratch_bytes(int64_t n) {
 void launch_rank(const double* d_records, const gvo_config* d_cfgs, int64_t n, int64_t* d_order,
                  void* d_scratch, cudaStream_t st) {
   if (n <= 0) return;
+  if (n <= kSmallRank) {
+    k_rank_small<<<1, 1024, 0, st>>>(d_records, d_cfgs, n, d_order);
+    return;
+  }
   const int64_t n_tiles = (n + kTile - 1) / kTile;
   uint8_t* p = (uint8_t*)d_scratch;
   uint64_t* k1 = (uint64_t*)p; p += n * 8;

@@ -42,6 +42,7 @@ struct UnitSh {
   int n_sub;
   uint32_t sub_mask[kMaxSub];
   int64_t sub_r[kMaxSub];
+  int sub_sh[kMaxSub];      // log2(sub_r) when a power of two, else -1
   int64_t sub_val[kMaxSub];
   int64_t g, R;
   int status;
@@ -206,6 +207,65 @@ __device__ inline void cover_and_emit(const RunSink& S, const Lat& L0, const int
   }
 }
 
+
+// Warp-cooperative version: the class's translates P[0..n) (n <= 64, sorted,
+// unique) live in shared memory.  Rays of one dimension are disjoint (every
+// point starts or continues exactly one maximal ray along that stride), so
+// all rays of a dimension are judged in parallel against the points not yet
+// covered by larger-stride rays; the same greedy as cover_and_emit.
+__device__ void cover_warp(const RunSink& S, const Lat& L0, const int64_t* P, int n, int tag,
+                           const Granule& G) {
+  const int lane = threadIdx.x & 31;
+  uint64_t req = n >= 64 ? ~0ull : ((1ull << n) - 1);
+  for (int d = L0.nd - 1; d >= 0 && req; --d) {
+    const int64_t s = (int64_t)L0.st[d];
+    uint64_t clear = 0;
+    for (int i = lane; i < n; i += 32) {
+      if (contains(P, n, P[i] - s)) continue;  // not a ray start
+      uint64_t mem = 1ull << i;
+      int len = 1, pos = i;
+      while (pos + 1 < n) {
+        // the successor v + s, if present, is after pos
+        const int64_t t = P[pos] + s;
+        int lo = pos + 1, hi = n - 1, f = -1;
+        while (lo <= hi) {
+          const int mid = (lo + hi) >> 1;
+          if (P[mid] == t) { f = mid; break; }
+          if (P[mid] < t) lo = mid + 1; else hi = mid - 1;
+        }
+        if (f < 0) break;
+        mem |= 1ull << f;
+        ++len;
+        pos = f;
+      }
+      if (len >= 2 && __popcll(mem & req) >= 2) {
+        Lat L = L0;
+        L.base = P[i];
+        L.ex[d] += len - 1;
+        emit_lattice(S, L, tag, G);
+        clear |= mem;
+      }
+    }
+    const unsigned lo32 = __reduce_or_sync(0xffffffffu, (unsigned)clear);
+    const unsigned hi32 = __reduce_or_sync(0xffffffffu, (unsigned)(clear >> 32));
+    req &= ~(((uint64_t)hi32 << 32) | lo32);
+  }
+  if (!req) return;
+  const unsigned __int128 tol = (unsigned __int128)L0.span + (uint64_t)G.g;
+  for (int i = lane; i < n; i += 32) {
+    if (i > 0 && (unsigned __int128)(uint64_t)(P[i] - P[i - 1]) <= tol) continue;  // not a cluster start
+    int j = i;
+    uint64_t mem = 1ull << i;
+    while (j + 1 < n && (unsigned __int128)(uint64_t)(P[j + 1] - P[j]) <= tol) { ++j; mem |= 1ull << j; }
+    if (mem & req) {
+      Lat L = L0;
+      L.base = P[i];
+      L.span = L0.span + (uint64_t)(P[j] - P[i]);
+      emit_lattice(S, L, tag, G);
+    }
+  }
+}
+
 // lattice of one coefficient vector over one block box, translation 0
 __device__ inline Lat box_lattice(const int64_t* c, const int32_t bd[3], const Box& b, const Granule& G) {
   Lat L;
@@ -237,12 +297,22 @@ __device__ inline Lat box_lattice(const int64_t* c, const int32_t bd[3], const B
 __device__ uint64_t* cta_sort(uint64_t* a, uint64_t* b, int64_t n, int bit0, int nbits,
                               uint32_t* hist /* kNW*256 */, uint32_t* tot /* 256 */) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t chunk = (((n + kNW - 1) / kNW) + 31) & ~int64_t(31);
+  const int64_t chunk = (((n + kNW - 1) / kNW) + 255) & ~int64_t(255);
   const int64_t beg = min(n, (int64_t)w * chunk), end = min(n, beg + chunk);
   for (int sh = bit0; sh < bit0 + nbits; sh += 8) {
     for (int i = threadIdx.x; i < kNW * 256; i += kNT) hist[i] = 0;
     __syncthreads();
-    for (int64_t i = beg + lane; i < end; i += 32) atomicAdd(&hist[w * 256 + ((a[i] >> sh) & 255)], 1u);
+    for (int64_t i0 = beg; i0 < end; i0 += 256) {
+      uint32_t dg[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t i = i0 + k * 32 + lane;
+        dg[k] = i < end ? (uint32_t)(a[i] >> sh) & 255u : 256u;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (dg[k] < 256u) atomicAdd(&hist[w * 256 + dg[k]], 1u);
+    }
     __syncthreads();
     if (threadIdx.x < 256) {
       const int d = threadIdx.x;
@@ -273,21 +343,30 @@ __device__ uint64_t* cta_sort(uint64_t* a, uint64_t* b, int64_t n, int bit0, int
       }
     }
     __syncthreads();
-    for (int64_t i0 = beg; i0 < end; i0 += 32) {
-      const int64_t i = i0 + lane;
-      const bool v = i < end;
-      const uint64_t e = v ? a[i] : 0;
-      const uint32_t d = (uint32_t)(e >> sh) & 255u;
-      const unsigned act = __ballot_sync(0xffffffffu, v);
-      unsigned peers = 0;
-      if (v) {
-        peers = __match_any_sync(act, d);
-        const uint32_t pos = hist[w * 256 + d] + __popc(peers & ((1u << lane) - 1u));
-        b[pos] = e;
+    for (int64_t i0 = beg; i0 < end; i0 += 256) {
+      uint64_t ev[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t i = i0 + k * 32 + lane;
+        ev[k] = i < end ? a[i] : 0;
       }
-      __syncwarp();
-      if (v && (31 - __clz(peers)) == lane) hist[w * 256 + d] += __popc(peers);
-      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t i = i0 + k * 32 + lane;
+        const bool v = i < end;
+        const unsigned act = __ballot_sync(0xffffffffu, v);
+        if (!act) break;
+        const uint32_t d = (uint32_t)(ev[k] >> sh) & 255u;
+        unsigned peers = 0;
+        if (v) {
+          peers = __match_any_sync(act, d);
+          const uint32_t pos = hist[w * 256 + d] + __popc(peers & ((1u << lane) - 1u));
+          b[pos] = ev[k];
+        }
+        __syncwarp();
+        if (v && (31 - __clz(peers)) == lane) hist[w * 256 + d] += __popc(peers);
+        __syncwarp();
+      }
     }
     __syncthreads();
     uint64_t* t = a; a = b; b = t;
@@ -296,77 +375,91 @@ __device__ uint64_t* cta_sort(uint64_t* a, uint64_t* b, int64_t n, int bit0, int
 }
 
 // ------------------------------------------------------------------ sweep
-// Union counts of tagged subsets over the sorted elements.  Each warp owns a
-// contiguous chunk; pass 1 finds per-warp maxima of the (masked, rescaled)
-// interval ends, pass 2 walks again with the carried running maximum.
+// Union counts of tagged subsets over the sorted elements in one pass pair.
+// Each warp owns a contiguous chunk, each lane a contiguous sub-chunk (odd
+// length: conflict-free 8-byte shared loads).  Pass 1: per-lane maxima of the
+// rescaled interval ends for every subset; warp and CTA exclusive max-scans
+// give each lane the running maximum R before its sub-chunk.  Pass 2: a
+// sequential walk adds max(0, hi - max(lo - 1, R)) per selected interval.
+constexpr int kSubGroup = 4;
 __device__ void sweep(const uint64_t* e, int64_t n, UnitSh& U, int64_t* wmax /* kMaxSub*kNW */) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t chunk = (((n + kNW - 1) / kNW) + 31) & ~int64_t(31);
+  const int64_t chunk = (n + kNW - 1) / kNW;
   const int64_t beg = min(n, (int64_t)w * chunk), end = min(n, beg + chunk);
-  const int ns = U.n_sub;
-  for (int s0 = 0; s0 < ns; s0 += 8) {
-    const int sn = min(8, ns - s0);
-    int64_t mx[8];
-    for (int q = 0; q < 8; ++q) mx[q] = -1;
-    for (int64_t i = beg + lane; i < end; i += 32) {
-      const uint64_t x = e[i];
-      const uint32_t tag = (uint32_t)(x & 31u);
-      const int64_t lo = (int64_t)(x >> kKeyShift);
-      const int64_t hi = lo + (int64_t)((x >> kTagBits) & kLenMask);
-      for (int q = 0; q < sn; ++q)
-        if ((U.sub_mask[s0 + q] >> tag) & 1u) mx[q] = max(mx[q], hi / U.sub_r[s0 + q]);
-    }
-    for (int q = 0; q < sn; ++q) {
-      int64_t v = mx[q];
-      for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-      if (lane == 0) wmax[(s0 + q) * kNW + w] = v;
-    }
-    __syncthreads();
-    int64_t carry[8], cnt[8];
-    for (int q = 0; q < sn; ++q) {
-      int64_t r = -1;
-      for (int k = 0; k < w; ++k) r = max(r, wmax[(s0 + q) * kNW + k]);
-      carry[q] = r;
+  int64_t sub = (end - beg + 31) / 32;
+  if (sub > 0 && !(sub & 1)) ++sub;
+  const int64_t lb = min(end, beg + lane * sub), le = min(end, lb + sub);
+  for (int s0 = 0; s0 < U.n_sub; s0 += kSubGroup) {
+    const int sn = min(kSubGroup, U.n_sub - s0);
+    uint32_t mask[kSubGroup];
+    int sh[kSubGroup];
+    int64_t r[kSubGroup], R[kSubGroup], cnt[kSubGroup];
+#pragma unroll
+    for (int q = 0; q < kSubGroup; ++q) {
+      mask[q] = q < sn ? U.sub_mask[s0 + q] : 0u;
+      sh[q] = q < sn ? U.sub_sh[s0 + q] : 0;
+      r[q] = q < sn ? U.sub_r[s0 + q] : 1;
+      R[q] = -1;
       cnt[q] = 0;
     }
-    for (int64_t i0 = beg; i0 < end; i0 += 32) {
-      const int64_t i = i0 + lane;
-      const bool v = i < end;
-      const uint64_t x = v ? e[i] : 0;
+    // pass 1: lane maxima
+    for (int64_t i = lb; i < le; ++i) {
+      const uint64_t x = e[i];
+      const uint32_t tag = (uint32_t)(x & 31u);
+      const int64_t hi0 = (int64_t)(x >> kKeyShift) + (int64_t)((x >> kTagBits) & kLenMask);
+#pragma unroll
+      for (int q = 0; q < kSubGroup; ++q)
+        if ((mask[q] >> tag) & 1u) R[q] = max(R[q], sh[q] >= 0 ? (hi0 >> sh[q]) : hi0 / r[q]);
+    }
+    // warp exclusive max-scan per subset; warp totals to shared memory
+#pragma unroll
+    for (int q = 0; q < kSubGroup; ++q) {
+      int64_t inc = R[q];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc = max(inc, t);
+      }
+      int64_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
+      if (lane == 0) ex = -1;
+      R[q] = ex;
+      if (lane == 31 && q < sn) wmax[q * kNW + w] = inc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kSubGroup; ++q) {
+      if (q >= sn) continue;
+      int64_t c = -1;
+      for (int k = 0; k < w; ++k) c = max(c, wmax[q * kNW + k]);
+      R[q] = max(R[q], c);
+    }
+    __syncthreads();
+    // pass 2: contributions
+    for (int64_t i = lb; i < le; ++i) {
+      const uint64_t x = e[i];
       const uint32_t tag = (uint32_t)(x & 31u);
       const int64_t lo0 = (int64_t)(x >> kKeyShift);
       const int64_t hi0 = lo0 + (int64_t)((x >> kTagBits) & kLenMask);
-      for (int q = 0; q < sn; ++q) {
-        const bool in = v && ((U.sub_mask[s0 + q] >> tag) & 1u);
-        const int64_t r = U.sub_r[s0 + q];
-        const int64_t lo = in ? lo0 / r : -1, hi = in ? hi0 / r : -1;
-        // inclusive max-scan of hi across lanes
-        int64_t inc = hi;
-        for (int o = 1; o < 32; o <<= 1) {
-          int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc = max(inc, t);
-        }
-        int64_t before = __shfl_up_sync(0xffffffffu, inc, 1);
-        if (lane == 0) before = -1;
-        before = max(before, carry[q]);
-        if (in) {
-          if (lo > before) cnt[q] += hi - lo + 1;
-          else if (hi > before) cnt[q] += hi - before;
-        }
-        carry[q] = max(carry[q], __shfl_sync(0xffffffffu, inc, 31));
+#pragma unroll
+      for (int q = 0; q < kSubGroup; ++q) {
+        if (!((mask[q] >> tag) & 1u)) continue;
+        const int64_t lo = sh[q] >= 0 ? (lo0 >> sh[q]) : lo0 / r[q];
+        const int64_t hi = sh[q] >= 0 ? (hi0 >> sh[q]) : hi0 / r[q];
+        if (lo > R[q]) cnt[q] += hi - lo + 1;
+        else if (hi > R[q]) cnt[q] += hi - R[q];
+        R[q] = max(R[q], hi);
       }
     }
-    __syncthreads();
-    for (int q = 0; q < sn; ++q) {
+#pragma unroll
+    for (int q = 0; q < kSubGroup; ++q) {
       int64_t v = cnt[q];
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) wmax[(s0 + q) * kNW + w] = v;
+      if (lane == 0 && q < sn) wmax[q * kNW + w] = v;
     }
     __syncthreads();
     if (threadIdx.x < sn) {
-      int64_t s = 0;
-      for (int k = 0; k < kNW; ++k) s += wmax[(s0 + threadIdx.x) * kNW + k];
-      U.sub_val[s0 + threadIdx.x] = s;
+      int64_t v = 0;
+      for (int k = 0; k < kNW; ++k) v += wmax[threadIdx.x * kNW + k];
+      U.sub_val[s0 + threadIdx.x] = v;
     }
     __syncthreads();
   }
@@ -379,6 +472,7 @@ struct SetsArgs {
   const gvo_config* cfgs;
   const Geo* geos;
   const int64_t* coefs;
+  const int64_t* ctabs;
   int64_t n_items;
   int S_req;
   int F_stride;
@@ -394,9 +488,11 @@ struct SetsArgs {
   int64_t run_cap;
   int64_t elem_cap;
   int* status_out;          // modes 1/2: unit status
+  int64_t* unit_stats;      // optional [n_items][10]: runs, N, smem?, cycles, key bits, sm, t_runs, t_emit, t_sort, t_sweep
+  unsigned long long* work; // dynamic work counter (zeroed before launch)
 };
 
-__global__ void __launch_bounds__(kNT) k_sets(SetsArgs P) {
+__global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
   extern __shared__ __align__(16) uint8_t smem[];
   UnitSh& U = *reinterpret_cast<UnitSh*>(smem);
   size_t off = (sizeof(UnitSh) + 15) & ~size_t(15);
@@ -404,6 +500,7 @@ __global__ void __launch_bounds__(kNT) k_sets(SetsArgs P) {
   uint32_t* tot = reinterpret_cast<uint32_t*>(smem + off); off += 256 * 4;
   int64_t* wmax = reinterpret_cast<int64_t*>(smem + off); off += kMaxSub * kNW * 8;
   int64_t* roff_sh = reinterpret_cast<int64_t*>(smem + off); off += (kSmemRuns + 1) * 8;
+  int64_t* cpts = reinterpret_cast<int64_t*>(smem + off); off += kNW * kClassPts * 8;
   uint64_t* ebuf = reinterpret_cast<uint64_t*>(smem + off);
   const int64_t sm_elems = (int64_t)(kSetsSmemBytes - off) / 16;
 
@@ -412,7 +509,14 @@ __global__ void __launch_bounds__(kNT) k_sets(SetsArgs P) {
   int64_t* roff_gl = reinterpret_cast<int64_t*>(slab + P.run_cap * sizeof(Run));
   uint64_t* gbuf = reinterpret_cast<uint64_t*>(slab + P.run_cap * sizeof(Run) + (P.run_cap + 1) * 8);
 
-  for (int64_t item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+  __shared__ int64_t next_item;
+  for (;;) {
+    // dynamic fetch: wave units (the heavy ones) are numbered first
+    if (threadIdx.x == 0) next_item = (int64_t)atomicAdd(P.work, 1ull);
+    __syncthreads();
+    const int64_t item = next_item;
+    if (item >= P.n_items) break;
+    const long long t_start = clock64();
     // ---------------- unit description
     if (threadIdx.x == 0) {
       U.status = GVO_OK;
@@ -425,10 +529,18 @@ __global__ void __launch_bounds__(kNT) k_sets(SetsArgs P) {
       int j = 0;
       bool skip = false;
       if (P.mode == 0) {
-        const int64_t per_cfg = (int64_t)P.F_stride * (P.S_req + 1);
-        c = item / per_cfg;
-        f = (item % per_cfg) / (P.S_req + 1);
-        j = (int)(item % (P.S_req + 1));
+        const int64_t n_cfg = P.n_items / ((int64_t)P.F_stride * (P.S_req + 1));
+        const int64_t n_wave = n_cfg * P.F_stride;
+        if (item < n_wave) {
+          c = item / P.F_stride;
+          f = item % P.F_stride;
+          j = P.S_req;
+        } else {
+          const int64_t r = item - n_wave;
+          c = r / ((int64_t)P.F_stride * P.S_req);
+          f = (r / P.S_req) % P.F_stride;
+          j = (int)(r % P.S_req);
+        }
       } else {
         c = 0;
         f = item;
@@ -441,7 +553,7 @@ __global__ void __launch_bounds__(kNT) k_sets(SetsArgs P) {
       U.field = (int)f;
       U.j = j;
       if (!skip && P.mode == 0 && j < P.S_req) {
-        if (j >= G.n_samples) skip = true;
+        if (j >= G.n_samples || G.dup_of[f][j] >= 0) skip = true;
         else {
           U.kind = 0;
           U.n_src = 2;
@@ -512,87 +624,86 @@ __global__ void __launch_bounds__(kNT) k_sets(SetsArgs P) {
       U.g = g;
       U.R = R;
       if (U.kind == 0) U.sub_r[1] = R;
+      for (int q = 0; q < U.n_sub; ++q) {
+        const int64_t r = U.sub_r[q];
+        int sh = -1;
+        if (r > 0 && (r & (r - 1)) == 0) { sh = 0; while ((int64_t(1) << sh) < r) ++sh; }
+        U.sub_sh[q] = sh;
+      }
     }
     const int64_t tpb = G.tpb;
     RunSink sink{runs, (int)P.run_cap, &U.n_runs, &U.status, &U.key_lo, &U.key_hi};
     __syncthreads();
 
-    // ---------------- run building: one thread per (source, box)
-    for (int task = threadIdx.x; task < U.n_src * 5; task += kNT) {
-      const int s = task / 5, bi = task % 5;
-      Box boxes[5];
-      const int nb = run_boxes(U.src_start[s], U.src_count[s], gd, boxes);
-      const int fk = P.T.fk_off[tpl * (2 * kMaxFields + 1) + U.field * 2 + U.src_kind[s]];
-      const int fk_end = P.T.fk_off[tpl * (2 * kMaxFields + 1) + U.field * 2 + U.src_kind[s] + 1];
-      const int na = fk_end - fk;
-      if (bi == 0) {  // points runs for non-affine accesses (whole source)
-        for (int q = 0; q < na; ++q) {
-          const int a = P.T.fk_list[fk + q];
-          if (crow[a * 8 + 7] == kAffine) continue;
-          int64_t clo[6], chi[6];
-          clo[0] = clo[1] = clo[2] = 0;
-          chi[0] = bd[0] - 1; chi[1] = bd[1] - 1; chi[2] = bd[2] - 1;
-          run_bid_bounds(U.src_start[s], U.src_count[s], gd, clo + 3, chi + 3);
-          int64_t lo, hi;
-          const int ga = abase + a;
-          bounds_check(P.T.code + P.T.code_off[ga], P.T.code_len[ga], clo, chi, bd, fbase, &lo, &hi);
-          const int slot = atomicAdd(&U.n_runs, 1);
-          if (slot >= P.run_cap) { atomicExch(&U.status, GVO_ERR_CAPACITY); continue; }
-          Run r;
-          r.kind = 1;
-          r.access = a;
-          r.tag = U.src_tag[s];
-          r.run_start = U.src_start[s];
-          r.run_count = U.src_count[s];
-          r.count = U.src_count[s] * tpb;
-          r.pieces = 1;
-          r.nd = 0;
-          r.base = 0;
-          r.span = 0;
-          runs[slot] = r;
-          atomicMin((long long*)&U.key_lo, (long long)Gr.of(lo));
-          atomicMax((long long*)&U.key_hi, (long long)Gr.of(hi));
-        }
-      }
-      if (bi >= nb) continue;
-      const Box box = boxes[bi];
-      // coefficient classes (accesses with identical thread/block coefficients)
-      uint32_t done[GVO_MAX_ACCESSES / 32];
-      for (int q = 0; q < (na + 31) / 32; ++q) done[q] = 0;
-      for (int q = 0; q < na; ++q) {
+    // ---------------- run building
+    // (a) points runs for non-affine accesses: one task per (source, access)
+    const int32_t* fko = P.T.fk_off + tpl * (2 * kMaxFields + 1);
+    for (int task = threadIdx.x; task < U.n_src * 64; task += kNT) {
+      const int s = task >> 6;
+      const int slot = U.field * 2 + U.src_kind[s];
+      const int fk = fko[slot], na = fko[slot + 1] - fk;
+      for (int q = task & 63; q < na; q += 64) {
         const int a = P.T.fk_list[fk + q];
-        if (crow[a * 8 + 7] != kAffine) continue;
-        if ((done[q >> 5] >> (q & 31)) & 1u) continue;
-        const int64_t* ca = crow + a * 8;
-        const Lat L0 = box_lattice(ca, bd, box, Gr);
-        int64_t pts[kClassPts];
-        int np = 0;
-        for (int q2 = q; q2 < na; ++q2) {
-          if ((done[q2 >> 5] >> (q2 & 31)) & 1u) continue;
-          const int a2 = P.T.fk_list[fk + q2];
-          const int64_t* cb = crow + a2 * 8;
-          if (cb[7] != kAffine) continue;
-          bool same = true;
-          for (int k = 1; k < 7; ++k) same &= cb[k] == ca[k];
-          if (!same) continue;
-          done[q2 >> 5] |= 1u << (q2 & 31);
-          // translate of L0 by the access constant
-          const int64_t p = (int64_t)((uint64_t)L0.base + (uint64_t)cb[0]);
-          // insertion into sorted unique list
-          int k = np;
-          bool dup = false;
-          while (k > 0 && pts[k - 1] >= p) { if (pts[k - 1] == p) { dup = true; break; } --k; }
-          if (dup) continue;
-          for (int m = np; m > k; --m) pts[m] = pts[m - 1];
-          pts[k] = p;
-          ++np;
-          if (np == kClassPts) { cover_and_emit(sink, L0, pts, np, U.src_tag[s], Gr); np = 0; }
+        if (crow[a * 8 + 7] == kAffine) continue;
+        int64_t clo[6], chi[6];
+        clo[0] = clo[1] = clo[2] = 0;
+        chi[0] = bd[0] - 1; chi[1] = bd[1] - 1; chi[2] = bd[2] - 1;
+        run_bid_bounds(U.src_start[s], U.src_count[s], gd, clo + 3, chi + 3);
+        int64_t lo, hi;
+        const int ga = abase + a;
+        bounds_check(P.T.code + P.T.code_off[ga], P.T.code_len[ga], clo, chi, bd, fbase, &lo, &hi);
+        const int slot_r = atomicAdd(&U.n_runs, 1);
+        if (slot_r >= P.run_cap) { atomicExch(&U.status, GVO_ERR_CAPACITY); continue; }
+        Run r;
+        r.kind = 1;
+        r.access = a;
+        r.tag = U.src_tag[s];
+        r.run_start = U.src_start[s];
+        r.run_count = U.src_count[s];
+        r.count = U.src_count[s] * tpb;
+        r.pieces = 1;
+        r.nd = 0;
+        r.base = 0;
+        r.span = 0;
+        runs[slot_r] = r;
+        atomicMin((long long*)&U.key_lo, (long long)Gr.of(lo));
+        atomicMax((long long*)&U.key_hi, (long long)Gr.of(hi));
+      }
+    }
+    // (b) lattices: one WARP per (source, box, coefficient class)
+    {
+      const CTab ct{const_cast<int64_t*>(P.ctabs) + c * ctab_stride(P.T.max_acc), P.T.max_acc};
+      const int slot0 = U.field * 2;
+      const int ncl0 = (int)(ct.slot_first()[slot0 + 1] - ct.slot_first()[slot0]);
+      const int ncl1 = (int)(ct.slot_first()[slot0 + 2] - ct.slot_first()[slot0 + 1]);
+      const int ncl = max(ncl0, ncl1);
+      const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      int64_t* wpts = cpts + wid * kClassPts;
+      for (int task = wid; task < U.n_src * 5 * ncl; task += kNW) {
+        const int s = task / (5 * ncl), rem = task % (5 * ncl), bi = rem / ncl, ci = rem % ncl;
+        const int slot = slot0 + U.src_kind[s];
+        const int64_t cl0 = ct.slot_first()[slot];
+        if (ci >= ct.slot_first()[slot + 1] - cl0) continue;
+        Box boxes[5];
+        const int nb = run_boxes(U.src_start[s], U.src_count[s], gd, boxes);
+        if (bi >= nb) continue;
+        const int64_t cls = cl0 + ci;
+        const int64_t* ca = crow + ct.rep()[cls] * 8;
+        const Lat L0 = box_lattice(ca, bd, boxes[bi], Gr);
+        const int64_t* cp = ct.pts() + ct.start()[cls];
+        const int64_t np = ct.cnt()[cls];
+        for (int64_t p0 = 0; p0 < np; p0 += kClassPts) {
+          const int m = (int)((np - p0) < kClassPts ? (np - p0) : kClassPts);
+          __syncwarp();
+          for (int k = lane; k < m; k += 32) wpts[k] = (int64_t)((uint64_t)L0.base + (uint64_t)cp[p0 + k]);
+          __syncwarp();
+          cover_warp(sink, L0, wpts, m, U.src_tag[s], Gr);
         }
-        if (np) cover_and_emit(sink, L0, pts, np, U.src_tag[s], Gr);
       }
     }
     __syncthreads();
 
+    const long long t_runs = clock64();
     // ---------------- offsets of runs, element count
     const int nr = min(U.n_runs, (int)P.run_cap);
     int64_t* roff = nr <= kSmemRuns ? roff_sh : roff_gl;
@@ -628,52 +739,74 @@ __global__ void __launch_bounds__(kNT) k_sets(SetsArgs P) {
     else { A0 = gbuf; B0 = gbuf + P.elem_cap; }
     const int64_t kbase = U.key_lo;
 
-    // ---------------- emission
-    for (int64_t i = threadIdx.x; i < N; i += kNT) {
-      int lo = 0, hi = nr - 1;
-      while (lo < hi) {  // last run with roff[r] <= i
-        int mid = (lo + hi + 1) >> 1;
-        if (roff[mid] <= i) lo = mid; else hi = mid - 1;
-      }
-      const Run& r = runs[lo];
-      int64_t k = i - roff[lo];
-      int64_t glo, ghi;
-      if (r.kind == 0) {
-        const int64_t piece = k % r.pieces;
-        k /= r.pieces;
-        uint64_t b = (uint64_t)r.base;
-        for (int d = r.nd - 1; d >= 0; --d) {
-          const int64_t idx = k % r.ext[d];
-          k /= r.ext[d];
-          b += (uint64_t)r.stride[d] * (uint64_t)idx;
+    // ---------------- emission: each thread owns a contiguous element range
+    // (one binary search for its first run, then a cursor), outer-tuple
+    // decode in 32-bit arithmetic when the run's extents allow it.
+    {
+      const int64_t per = (N + kNT - 1) / kNT;
+      const int64_t e0 = min(N, (int64_t)threadIdx.x * per), e1 = min(N, e0 + per);
+      int ri = 0;
+      if (e0 < e1) {
+        int lo = 0, hi = nr - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (roff[mid] <= e0) lo = mid; else hi = mid - 1;
         }
-        glo = Gr.of((int64_t)b);
-        ghi = Gr.of((int64_t)(b + r.span));
-        if (r.pieces > 1) {
-          int64_t plo = glo + piece * kPiece;
-          if (plo > ghi) plo = glo;
-          const int64_t phi = min(ghi, plo + kPiece - 1);
-          glo = plo;
-          ghi = phi;
-        }
-      } else {
-        const int64_t blk = r.run_start + k / tpb;
-        const int64_t th = k % tpb;
-        int64_t crd[6];
-        crd[0] = th % bd[0];
-        crd[1] = (th / bd[0]) % bd[1];
-        crd[2] = th / ((int64_t)bd[0] * bd[1]);
-        crd[3] = blk % gd[0];
-        crd[4] = (blk / gd[0]) % gd[1];
-        crd[5] = blk / (gd[0] * gd[1]);
-        const int ga = abase + r.access;
-        glo = ghi = Gr.of(eval_point(P.T.code + P.T.code_off[ga], P.T.code_len[ga], crd, bd, fbase));
+        ri = lo;
       }
-      A0[i] = ((uint64_t)(glo - kbase) << kKeyShift) | ((uint64_t)(ghi - glo) << kTagBits) |
-              (uint64_t)r.tag;
+      for (int64_t i = e0; i < e1; ++i) {
+        while (roff[ri + 1] <= i) ++ri;
+        const Run& r = runs[ri];
+        int64_t k = i - roff[ri];
+        int64_t glo, ghi;
+        if (r.kind == 0) {
+          int64_t piece = 0;
+          if (r.pieces > 1) { piece = k % r.pieces; k /= r.pieces; }
+          uint64_t b = (uint64_t)r.base;
+          if (k < (int64_t(1) << 31)) {
+            uint32_t k32 = (uint32_t)k;
+            for (int d = r.nd - 1; d >= 0; --d) {
+              const uint32_t ex = (uint32_t)r.ext[d];
+              const uint32_t q = ex ? k32 / ex : 0;
+              b += (uint64_t)r.stride[d] * (uint64_t)(k32 - q * ex);
+              k32 = q;
+            }
+          } else {
+            for (int d = r.nd - 1; d >= 0; --d) {
+              const int64_t idx = k % r.ext[d];
+              k /= r.ext[d];
+              b += (uint64_t)r.stride[d] * (uint64_t)idx;
+            }
+          }
+          glo = Gr.of((int64_t)b);
+          ghi = Gr.of((int64_t)(b + r.span));
+          if (r.pieces > 1) {
+            int64_t plo = glo + piece * kPiece;
+            if (plo > ghi) plo = glo;
+            const int64_t phi = min(ghi, plo + kPiece - 1);
+            glo = plo;
+            ghi = phi;
+          }
+        } else {
+          const int64_t blk = r.run_start + k / tpb;
+          const int64_t th = k % tpb;
+          int64_t crd[6];
+          crd[0] = th % bd[0];
+          crd[1] = (th / bd[0]) % bd[1];
+          crd[2] = th / ((int64_t)bd[0] * bd[1]);
+          crd[3] = blk % gd[0];
+          crd[4] = (blk / gd[0]) % gd[1];
+          crd[5] = blk / (gd[0] * gd[1]);
+          const int ga = abase + r.access;
+          glo = ghi = Gr.of(eval_point(P.T.code + P.T.code_off[ga], P.T.code_len[ga], crd, bd, fbase));
+        }
+        A0[i] = ((uint64_t)(glo - kbase) << kKeyShift) | ((uint64_t)(ghi - glo) << kTagBits) |
+                (uint64_t)r.tag;
+      }
     }
     __syncthreads();
 
+    const long long t_emit = clock64();
     // ---------------- sort + sweeps
     int kb = 0;
     {
@@ -682,9 +815,26 @@ __global__ void __launch_bounds__(kNT) k_sets(SetsArgs P) {
     }
     const int nbits = ((kb + 7) / 8) * 8;
     const uint64_t* sorted = cta_sort(A0, B0, N, kKeyShift, nbits, hist, tot);
+    const long long t_sort = clock64();
     sweep(sorted, N, U, wmax);
+    const long long t_sweep = clock64();
 
     // ---------------- outputs
+    if (threadIdx.x == 0 && P.unit_stats) {
+      int64_t* us = P.unit_stats + item * 10;
+      us[6] = t_runs - t_start;
+      us[7] = t_emit - t_runs;
+      us[8] = t_sort - t_emit;
+      us[9] = t_sweep - t_sort;
+      us[0] = nr;
+      us[1] = N;
+      us[2] = N <= sm_elems;
+      us[3] = clock64() - t_start;
+      us[4] = nbits;
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      us[5] = smid;
+    }
     if (threadIdx.x == 0) {
       const int f = U.field;
       if (P.mode == 0) {
@@ -728,6 +878,7 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st) {
   P.cfgs = L.cfgs;
   P.geos = L.geos;
   P.coefs = L.coefs;
+  P.ctabs = L.ctabs;
   P.n_items = L.n_items;
   P.S_req = L.S_req;
   P.F_stride = L.F_stride;
@@ -743,7 +894,10 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st) {
   P.run_cap = L.run_cap;
   P.elem_cap = L.elem_cap;
   P.status_out = L.status_out;
+  P.unit_stats = L.unit_stats;
+  P.work = L.work;
   if (P.n_items <= 0) return;
+  cudaMemsetAsync(P.work, 0, sizeof(unsigned long long), st);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sets, cudaFuncAttributeMaxDynamicSharedMemorySize, kSetsSmemBytes);

@@ -54,8 +54,82 @@ __device__ inline int representative(const int64_t g[3], int samples, int64_t* o
   return cnt;
 }
 
+// Coefficient classes of every (field, kind) slot (one warp).  Lanes find
+// each access's representative (first earlier access of the slot with the
+// same coefficients); lane 0 numbers the classes in slot order; lanes then
+// gather each class's constants and sort them (insertion sort, unique).
+__device__ void build_classes(const TplView& T, int tpl, const int64_t* crow, CTab ct, int16_t* rep_of) {
+  const int lane = threadIdx.x & 31;
+  const int32_t* fko = T.fk_off + tpl * (2 * kMaxFields + 1);
+  for (int slot = 0; slot < 2 * kMaxFields; ++slot) {
+    const int b = fko[slot], e = fko[slot + 1];
+    for (int q = b + lane; q < e; q += 32) {
+      const int a = T.fk_list[q];
+      const int64_t* ca = crow + a * 8;
+      int64_t r = -1;
+      if (ca[7] == kAffine) {
+        r = a;
+        for (int q2 = b; q2 < q; ++q2) {
+          const int a2 = T.fk_list[q2];
+          const int64_t* cb = crow + a2 * 8;
+          if (cb[7] != kAffine) continue;
+          bool same = true;
+          for (int k = 1; k < 7; ++k) same &= cb[k] == ca[k];
+          if (same) { r = a2; break; }
+        }
+      }
+      rep_of[a] = (int16_t)r;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    int64_t ncls = 0, off = 0;
+    for (int slot = 0; slot < 2 * kMaxFields; ++slot) {
+      ct.slot_first()[slot] = ncls;
+      const int b = fko[slot], e = fko[slot + 1];
+      for (int q = b; q < e; ++q) {
+        const int a = T.fk_list[q];
+        if (rep_of[a] != a) continue;
+        int64_t members = 0;
+        for (int q2 = q; q2 < e; ++q2) members += rep_of[T.fk_list[q2]] == a;
+        ct.rep()[ncls] = a;
+        ct.start()[ncls] = off;
+        ct.cnt()[ncls] = members;
+        off += members;
+        ++ncls;
+      }
+    }
+    ct.slot_first()[2 * kMaxFields] = ncls;
+  }
+  __syncwarp();
+  const int64_t ncls = ct.slot_first()[2 * kMaxFields];
+  for (int64_t c = lane; c < ncls; c += 32) {
+    const int64_t r = ct.rep()[c];
+    const int f = T.acc_field[T.acc_base[tpl] + r], k = T.acc_kind[T.acc_base[tpl] + r];
+    const int b = fko[f * 2 + k], e = fko[f * 2 + k + 1];
+    int64_t* P = ct.pts() + ct.start()[c];
+    int64_t n = 0;
+    for (int q = b; q < e; ++q) {
+      const int a = T.fk_list[q];
+      if (rep_of[a] != r) continue;
+      const int64_t v = crow[a * 8];
+      int64_t j = n;
+      bool dup = false;
+      while (j > 0 && P[j - 1] >= v) {
+        if (P[j - 1] == v) { dup = true; break; }
+        --j;
+      }
+      if (dup) continue;
+      for (int64_t m = n; m > j; --m) P[m] = P[m - 1];
+      P[j] = v;
+      ++n;
+    }
+    ct.cnt()[c] = n;
+  }
+}
+
 __global__ void k_setup(TplView T, const gvo_machine* machines, const gvo_config* cfgs,
-                        int64_t n, gvo_sampling smp, int64_t* coefs, Geo* geos) {
+                        int64_t n, gvo_sampling smp, int64_t* coefs, Geo* geos, int64_t* ctabs) {
   const int lane = threadIdx.x & 31;
   const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= n) return;
@@ -77,6 +151,12 @@ __global__ void k_setup(TplView T, const gvo_machine* machines, const gvo_config
     int flag = affine_extract(T.code + T.code_off[ga], T.code_len[ga], bd, fbase, &f);
     for (int k = 0; k < 7; ++k) crow[a * 8 + k] = flag == kAffine ? f.c[k] : 0;
     crow[a * 8 + 7] = flag;
+  }
+  __syncwarp();
+  {
+    extern __shared__ int16_t sh_rep[];
+    build_classes(T, tpl, crow, CTab{ctabs + c * ctab_stride(T.max_acc), T.max_acc},
+                  sh_rep + (threadIdx.x >> 5) * T.max_acc);
   }
 
   // ---- geometry (computed redundantly by every lane; cheap and uniform)
@@ -143,6 +223,38 @@ __global__ void k_setup(TplView T, const gvo_machine* machines, const gvo_config
     int ns = representative(gd, smp.block_samples, G.sample_lin, kMaxSamples);
     if (ns < 0) fail(GVO_ERR_UNSUPPORTED, 0, -1, 0);
     else G.n_samples = ns;
+  }
+  // ---- translation dedup of block samples (exact): all accesses of field f
+  // affine with one common block-coordinate coefficient vector, and the
+  // address shift between samples j and j' a multiple of the line size.
+  for (int f = 0; f < kMaxFields; ++f)
+    for (int j = 0; j < kMaxSamples; ++j) G.dup_of[f][j] = -1;
+  if (G.status == GVO_OK && (G.phases & 1)) {
+    const int32_t* fko = T.fk_off + tpl * (2 * kMaxFields + 1);
+    for (int f = 0; f < F; ++f) {
+      bool ok = true;
+      const int64_t* c0 = nullptr;
+      for (int q = fko[2 * f]; q < fko[2 * f + 2] && ok; ++q) {
+        const int64_t* ca = crow + T.fk_list[q] * 8;
+        if (ca[7] != kAffine) { ok = false; break; }
+        if (!c0) c0 = ca;
+        else ok = ca[4] == c0[4] && ca[5] == c0[5] && ca[6] == c0[6];
+      }
+      if (!ok || !c0) continue;
+      const int64_t line = m.l1_line_bytes;
+      for (int j = 1; j < G.n_samples; ++j) {
+        const int64_t bj = G.sample_lin[j];
+        const int64_t xj = bj % gd[0], yj = (bj / gd[0]) % gd[1], zj = bj / (gd[0] * gd[1]);
+        for (int i = 0; i < j; ++i) {
+          if (G.dup_of[f][i] >= 0) continue;
+          const int64_t bi = G.sample_lin[i];
+          const int64_t xi = bi % gd[0], yi = (bi / gd[0]) % gd[1], zi = bi / (gd[0] * gd[1]);
+          const __int128 d = (__int128)c0[4] * (xj - xi) + (__int128)c0[5] * (yj - yi) + (__int128)c0[6] * (zj - zi);
+          const __int128 r = d % line;
+          if (r == 0) { G.dup_of[f][j] = (int8_t)i; break; }
+        }
+      }
+    }
   }
   if (G.status == GVO_OK && (G.phases & 1)) {
     for (int s = 0; s < G.n_samples; ++s) {
@@ -220,11 +332,29 @@ __global__ void k_setup(TplView T, const gvo_machine* machines, const gvo_config
 }
 
 void launch_setup(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs,
-                  int64_t n, const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos,
+                  int64_t n, const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos, int64_t* d_ctabs,
                   cudaStream_t st) {
   const int wpb = 4;
   const int64_t blocks = (n + wpb - 1) / wpb;
-  if (blocks > 0) k_setup<<<(unsigned)blocks, wpb * 32, 0, st>>>(T, d_machines, d_cfgs, n, smp, d_coefs, d_geos);
+  if (blocks > 0)
+    k_setup<<<(unsigned)blocks, wpb * 32, wpb * T.max_acc * sizeof(int16_t), st>>>(T, d_machines, d_cfgs, n, smp,
+                                                                                   d_coefs, d_geos, d_ctabs);
+}
+
+__global__ void k_classes_only(TplView T, const gvo_config* cfgs, int64_t n, const int64_t* coefs,
+                               int64_t* ctabs) {
+  const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= n) return;
+  extern __shared__ int16_t sh_rep2[];
+  build_classes(T, cfgs[c].template_id, coefs + c * (int64_t)T.max_acc * 8,
+                CTab{ctabs + c * ctab_stride(T.max_acc), T.max_acc}, sh_rep2 + (threadIdx.x >> 5) * T.max_acc);
+}
+
+void launch_classes(const TplView& T, const gvo_config* d_cfgs, int64_t n, const int64_t* d_coefs,
+                    int64_t* d_ctabs, cudaStream_t st) {
+  if (n > 0)
+    k_classes_only<<<(unsigned)((n + 3) / 4), 128, 4 * T.max_acc * sizeof(int16_t), st>>>(T, d_cfgs, n, d_coefs,
+                                                                                          d_ctabs);
 }
 
 }  // namespace gvo

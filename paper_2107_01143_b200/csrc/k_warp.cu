@@ -89,24 +89,51 @@ __global__ void __launch_bounds__(256) k_warp(TplView T, const gvo_machine* mach
     const Granule G = Granule::make(is_l1 ? bw : sec);
 
     for (int i = threadIdx.x; i < 2 * kMaxFields + 3 * A; i += blockDim.x) sh[i] = 0;
+    // stage this config's coefficient rows (8 x int64 per access) in shared memory
+    int64_t* scoef = reinterpret_cast<int64_t*>(acc_l1 + 3 * A);
+    for (int i = threadIdx.x; i < 8 * A; i += blockDim.x) scoef[i] = crow[i];
+    uint32_t skip_field = 0;  // fields whose sample is a translate of an earlier one
+    if (mode == 0 && !is_l1)
+      for (int f = 0; f < kMaxFields; ++f) skip_field |= (geos[c].dup_of[f][j] >= 0 ? 1u : 0u) << f;
     __syncthreads();
 
-    for (int64_t t = wid; t < nw * A; t += nwarps) {
-      const int a = (int)(t % A);
+    // each hardware warp owns a contiguous range of (modelled warp, access)
+    // tasks, so thread coordinates are recomputed only when the warp changes
+    const int64_t ntask = nw * A;
+    const int64_t per = (ntask + nwarps - 1) / nwarps;
+    const int64_t t0 = wid * per, t1 = min(ntask, t0 + per);
+    int64_t cur_w = -1;
+    int64_t crd[6];
+    bool act = false;
+    unsigned am = 0;
+    for (int64_t t = t0; t < t1; ++t) {
       const int64_t w = t / A;
-      const int64_t th = w * 32 + lane;
-      const bool act = th < tpb;
-      const unsigned am = __ballot_sync(0xffffffffu, act);
-      int64_t crd[6];
-      crd[0] = th % bd[0];
-      crd[1] = (th / bd[0]) % bd[1];
-      crd[2] = th / ((int64_t)bd[0] * bd[1]);
-      crd[3] = bc[0]; crd[4] = bc[1]; crd[5] = bc[2];
+      const int a = (int)(t - w * A);
+      if (w != cur_w) {
+        cur_w = w;
+        const int64_t th = w * 32 + lane;
+        act = th < tpb;
+        am = __ballot_sync(0xffffffffu, act);
+        crd[0] = th % bd[0];
+        crd[1] = (th / bd[0]) % bd[1];
+        crd[2] = th / ((int64_t)bd[0] * bd[1]);
+        crd[3] = bc[0]; crd[4] = bc[1]; crd[5] = bc[2];
+      }
       const int ga = abase + a;
+      const int fa = T.acc_field[ga];
+      if ((skip_field >> fa) & 1u) continue;
       int64_t gid = 0;
       if (act) {
-        const int64_t addr = access_address(crow + a * 8, T.code + T.code_off[ga], T.code_len[ga],
-                                            crd, bd, fbase);
+        const int64_t* cf = scoef + a * 8;
+        int64_t addr;
+        if (cf[7] == kAffine) {
+          uint64_t v = (uint64_t)cf[0];
+#pragma unroll
+          for (int k = 0; k < 6; ++k) v += (uint64_t)cf[1 + k] * (uint64_t)crd[k];
+          addr = (int64_t)v;
+        } else {
+          addr = eval_point(T.code + T.code_off[ga], T.code_len[ga], crd, bd, fbase);
+        }
         gid = G.of(addr);
       }
       // distinct granules of the warp
@@ -115,7 +142,7 @@ __global__ void __launch_bounds__(256) k_warp(TplView T, const gvo_machine* mach
       const int distinct = __popc(__ballot_sync(0xffffffffu, lead));
       if (!is_l1) {
         if (lane == 0) {
-          const int slot = T.acc_field[ga] * 2 + T.acc_kind[ga];
+          const int slot = fa * 2 + T.acc_kind[ga];
           atomicAdd(&acc_fk[slot], (unsigned long long)(T.acc_mult[ga] * distinct));
         }
         continue;
@@ -195,7 +222,7 @@ void launch_warp(const TplView& T, const gvo_machine* d_machines, const gvo_conf
                  int F_stride, int64_t* d_l1_access, int32_t l1_stride, unsigned long long* d_out,
                  int max_acc, int n_sm, cudaStream_t st) {
   if (n_items <= 0) return;
-  const size_t smem = (2 * kMaxFields + 3 * (size_t)max_acc) * sizeof(unsigned long long);
+  const size_t smem = (2 * kMaxFields + 3 * (size_t)max_acc + 8 * (size_t)max_acc) * sizeof(unsigned long long);
   int64_t grid = n_items < (int64_t)n_sm * 8 ? n_items : (int64_t)n_sm * 8;
   k_warp<<<(unsigned)grid, 256, smem, st>>>(T, d_machines, d_cfgs, d_geos, d_coefs, n_items, S_req, sector,
                                              bank_width, n_banks, mode, d_block_list, d_counts,
