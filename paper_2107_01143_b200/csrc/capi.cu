@@ -279,6 +279,9 @@ int gvo_set_templates(gvo_ctx* ctx, const gvo_template* t, int32_t n) {
   V.field_base = ctx->t_fb.p; V.acc_field = ctx->t_af.p; V.acc_kind = ctx->t_ak.p; V.acc_mult = ctx->t_am.p;
   V.code_off = ctx->t_co.p; V.code_len = ctx->t_cl.p; V.code = ctx->t_code.p;
   V.fk_off = ctx->t_fko.p; V.fk_list = ctx->t_fkl.p; V.max_acc = maxa;
+  // pageable cudaMemcpy may return before its DMA lands, and the pipeline
+  // runs on non-blocking streams: make the upload visible to every stream
+  CK(cudaDeviceSynchronize());
   return GVO_OK;
 }
 
@@ -293,6 +296,7 @@ int gvo_set_machines(gvo_ctx* ctx, const gvo_machine* m, int32_t n) {
   ctx->h_machines.assign(m, m + n);
   if (!ctx->d_machines.ensure(n)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
   CK(cudaMemcpy(ctx->d_machines.p, m, n * sizeof(gvo_machine), cudaMemcpyHostToDevice));
+  CK(cudaDeviceSynchronize());
   return GVO_OK;
 }
 
@@ -343,12 +347,20 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     tmark_begin(ctx, 0, st, &tb);
     launch_setup(ctx->view, ctx->d_machines.p, cf, nb, *sampling, ctx->coefs.p, ctx->geos.p, ctx->ctabs.p, st);
     tmark_end(ctx, 0, st, tb);
-    tmark_begin(ctx, 1, st, &tb);
-    launch_warp(ctx->view, ctx->d_machines.p, cf, ctx->geos.p, ctx->coefs.p, nb * (S + 1), S, m0.sector_bytes,
-                m0.bank_width_bytes, m0.l1_banks, 0, nullptr, cnt, stride, F,
-                d_l1_access ? d_l1_access + b0 * l1_stride * 3 : nullptr, l1_stride, nullptr,
-                ctx->max_acc, ctx->n_sm, st);
-    tmark_end(ctx, 1, st, tb);
+    // warp statistics: fused into the k_sets work queue when their shared
+    // memory fits the set kernel's element buffer, else a separate launch
+    WarpArgs WA{ctx->view, ctx->d_machines.p, cf, ctx->geos.p, ctx->coefs.p, nb * (S + 1), S, m0.sector_bytes,
+               m0.bank_width_bytes, m0.l1_banks, 0, nullptr, cnt, stride, F,
+               d_l1_access ? d_l1_access + b0 * l1_stride * 3 : nullptr, l1_stride, nullptr};
+    const bool fuse = (int64_t)warp_item_smem(ctx->max_acc) <= sets_ebuf_bytes();
+    if (!fuse) {
+      tmark_begin(ctx, 1, st, &tb);
+      launch_warp(ctx->view, ctx->d_machines.p, cf, ctx->geos.p, ctx->coefs.p, nb * (S + 1), S, m0.sector_bytes,
+                  m0.bank_width_bytes, m0.l1_banks, 0, nullptr, cnt, stride, F,
+                  d_l1_access ? d_l1_access + b0 * l1_stride * 3 : nullptr, l1_stride, nullptr,
+                  ctx->max_acc, ctx->n_sm, st);
+      tmark_end(ctx, 1, st, tb);
+    }
     SetsLaunch L{};
     L.T = ctx->view;
     L.machines = ctx->d_machines.p;
@@ -369,7 +381,10 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     L.status_out = ctx->status.p;
     L.n_ctas = ctx->n_ctas;
     L.work = ctx->work.p;
-  L.work = ctx->work.p;
+    if (fuse) {
+      L.warp = WA;
+      L.n_warp_items = WA.n_items;
+    }
     if (ctx->unit_debug) {
       if (!ctx->unit_stats.ensure((size_t)L.n_items * 10)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
       CK(cudaMemsetAsync(ctx->unit_stats.p, 0, (size_t)L.n_items * 10 * 8, st));

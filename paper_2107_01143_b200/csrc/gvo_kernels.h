@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include "gvo_common.cuh"
+#include "gvo_warp.cuh"
 
 namespace gvo {
 
@@ -45,7 +46,10 @@ struct SetsLaunch {
   int n_ctas;
   int64_t* unit_stats = nullptr;
   unsigned long long* work = nullptr;
+  WarpArgs warp{};
+  int64_t n_warp_items = 0;
 };
+int64_t sets_ebuf_bytes();
 void launch_sets(const SetsLaunch& L, cudaStream_t st);
 int64_t sets_slab_bytes(int64_t run_cap, int64_t elem_cap);
 

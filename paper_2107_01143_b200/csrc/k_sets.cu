@@ -21,6 +21,7 @@
 // address sampling, no hashing.
 #include "gvo_bytecode.cuh"
 #include "gvo_kernels.h"
+#include "gvo_warp.cuh"
 
 namespace gvo {
 
@@ -490,6 +491,8 @@ struct SetsArgs {
   int* status_out;          // modes 1/2: unit status
   int64_t* unit_stats;      // optional [n_items][10]: runs, N, smem?, cycles, key bits, sm, t_runs, t_emit, t_sort, t_sweep
   unsigned long long* work; // dynamic work counter (zeroed before launch)
+  WarpArgs warp;            // fused warp-statistics items (appended after the set units)
+  int64_t n_warp_items;
 };
 
 __global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
@@ -515,7 +518,12 @@ __global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
     if (threadIdx.x == 0) next_item = (int64_t)atomicAdd(P.work, 1ull);
     __syncthreads();
     const int64_t item = next_item;
-    if (item >= P.n_items) break;
+    if (item >= P.n_items + P.n_warp_items) break;
+    if (item >= P.n_items) {
+      warp_item(P.warp, item - P.n_items, reinterpret_cast<unsigned long long*>(ebuf));
+      __syncthreads();
+      continue;
+    }
     const long long t_start = clock64();
     // ---------------- unit description
     if (threadIdx.x == 0) {
@@ -896,15 +904,25 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st) {
   P.status_out = L.status_out;
   P.unit_stats = L.unit_stats;
   P.work = L.work;
-  if (P.n_items <= 0) return;
+  P.warp = L.warp;
+  P.n_warp_items = L.n_warp_items;
+  if (P.n_items + P.n_warp_items <= 0) return;
   cudaMemsetAsync(P.work, 0, sizeof(unsigned long long), st);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sets, cudaFuncAttributeMaxDynamicSharedMemorySize, kSetsSmemBytes);
     attr = true;
   }
-  const int64_t grid = P.n_items < L.n_ctas ? P.n_items : L.n_ctas;
+  const int64_t tot = P.n_items + P.n_warp_items;
+  const int64_t grid = tot < L.n_ctas ? tot : L.n_ctas;
   k_sets<<<(unsigned)grid, kNT, kSetsSmemBytes, st>>>(P);
+}
+
+// bytes of the shared element buffer (what a fused warp item may use)
+int64_t sets_ebuf_bytes() {
+  size_t off = (sizeof(UnitSh) + 15) & ~size_t(15);
+  off += kNW * 256 * 4 + 256 * 4 + kMaxSub * kNW * 8 + (kSmemRuns + 1) * 8 + kNW * kClassPts * 8;
+  return (int64_t)kSetsSmemBytes - (int64_t)off;
 }
 
 int64_t sets_slab_bytes(int64_t run_cap, int64_t elem_cap) {
