@@ -90,6 +90,11 @@ struct gvo_ctx {
   int n_ctas = 0;
   DBuf<int> status;
   DBuf<unsigned long long> work;
+  // key-range splitting state: header + queue + descriptor arena
+  DBuf<uint8_t> split_mem;
+  SplitState* split = nullptr;
+  int64_t split_qcap = 1 << 16, split_arena = 64ll << 20;
+  int64_t sm_cap = 0;  // GVO_SMEM_ELEMS test hook
   DBuf<uint8_t> rank_scratch;
   // host-variant staging
   DBuf<gvo_config> s_cfgs;
@@ -157,6 +162,7 @@ int gvo_open(int device, gvo_ctx** out) {
   if (const char* e = getenv("GVO_ELEM_CAP")) ctx->elem_cap = atoll(e);
   if (const char* e = getenv("GVO_RUN_CAP")) ctx->run_cap = atoll(e);
   if (const char* e = getenv("GVO_BATCH")) ctx->batch = atoll(e);
+  if (const char* e = getenv("GVO_SMEM_ELEMS")) ctx->sm_cap = atoll(e);
   ctx->n_ctas = 2 * ctx->n_sm;
   *out = ctx;
   return GVO_OK;
@@ -176,6 +182,7 @@ void gvo_close(gvo_ctx* ctx) {
   ctx->geos.release();
   ctx->slab.release();
   ctx->status.release();
+  ctx->split_mem.release();
   ctx->rank_scratch.release();
   ctx->s_cfgs.release();
   ctx->s_counts.release();
@@ -310,6 +317,20 @@ static int ensure_work(gvo_ctx* ctx, int64_t n) {
       return set_err(ctx, GVO_ERR_CUDA, "scratch slab alloc failed%s");
   }
   if (!ctx->status.ensure(4) || !ctx->work.ensure(1)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
+  if (!ctx->split) {
+    const size_t hdr = 256;
+    const size_t qb = (size_t)ctx->split_qcap * sizeof(RangeItem);
+    if (!ctx->split_mem.ensure(hdr + qb + (size_t)ctx->split_arena)) return set_err(ctx, GVO_ERR_CUDA, "split alloc failed%s");
+    SplitState h{};
+    h.q_cap = ctx->split_qcap;
+    h.arena_bytes = ctx->split_arena;
+    h.queue = reinterpret_cast<RangeItem*>(ctx->split_mem.p + hdr);
+    h.arena = ctx->split_mem.p + hdr + qb;
+    CK(cudaMemset(ctx->split_mem.p, 0, hdr + qb));
+    CK(cudaMemcpy(ctx->split_mem.p, &h, sizeof h, cudaMemcpyHostToDevice));
+    CK(cudaDeviceSynchronize());
+    ctx->split = reinterpret_cast<SplitState*>(ctx->split_mem.p);
+  }
   return GVO_OK;
 }
 
@@ -381,13 +402,15 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     L.status_out = ctx->status.p;
     L.n_ctas = ctx->n_ctas;
     L.work = ctx->work.p;
+    L.split = ctx->split;
+    L.sm_cap = ctx->sm_cap;
     if (fuse) {
       L.warp = WA;
       L.n_warp_items = WA.n_items;
     }
     if (ctx->unit_debug) {
-      if (!ctx->unit_stats.ensure((size_t)L.n_items * 10)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
-      CK(cudaMemsetAsync(ctx->unit_stats.p, 0, (size_t)L.n_items * 10 * 8, st));
+      if (!ctx->unit_stats.ensure((size_t)L.n_items * 10 + 10 + 4096 * 10)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
+      CK(cudaMemsetAsync(ctx->unit_stats.p, 0, ((size_t)L.n_items * 10 + 10 + 4096 * 10) * 8, st));
       L.unit_stats = ctx->unit_stats.p;
       ctx->unit_items = L.n_items;
     }
@@ -519,6 +542,8 @@ int gvo_group_footprint(gvo_ctx* ctx, int32_t tpl, const int32_t block[3], const
   L.status_out = ctx->status.p;
   L.n_ctas = ctx->n_ctas;
   L.work = ctx->work.p;
+  L.split = ctx->split;
+    L.sm_cap = ctx->sm_cap;
   launch_sets(L, st);
   launch_warp(ctx->view, ctx->d_machines.p, ctx->s_cfgs.p, ctx->geos.p, ctx->coefs.p, (int64_t)blocks.size(), 0, granularity, 1, 1, 1,
               ctx->s_i64c.p, nullptr, 0, F, nullptr, 0, ctx->s_ull.p, ctx->max_acc, ctx->n_sm, st);
@@ -580,6 +605,8 @@ int gvo_group_sets(gvo_ctx* ctx, int32_t tpl, const int32_t block[3], const int6
   L.status_out = ctx->status.p;
   L.n_ctas = ctx->n_ctas;
   L.work = ctx->work.p;
+  L.split = ctx->split;
+    L.sm_cap = ctx->sm_cap;
   launch_sets(L, st);
   CK(cudaGetLastError());
   int status = 0;
@@ -686,7 +713,7 @@ int gvo_debug_units(gvo_ctx* ctx, int enable, int64_t* h_out, int64_t cap, int64
   if (n_items) *n_items = ctx->unit_items;
   if (h_out && ctx->unit_items) {
     CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(h_out, ctx->unit_stats.p, std::min<int64_t>(cap, ctx->unit_items) * 10 * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(h_out, ctx->unit_stats.p, std::min<int64_t>(cap, ctx->unit_items * 10 + 10 + 4096 * 10) * 8, cudaMemcpyDeviceToHost));
   }
   return GVO_OK;
 }

@@ -202,6 +202,9 @@ struct Run {
   int32_t tag;
   int32_t kind;     // 0 lattice, 1 points
   int32_t access;   // template-local access index (points runs)
+  int32_t mono;     // lattice whose interval starts/ends increase with the
+                    // tuple index (dim 0 fastest): range counts by bisection
+  int32_t pad_;
   int64_t count;    // intervals emitted by this run (incl. splitting)
   int64_t pieces;   // pieces per interval (long intervals are split)
   int64_t run_start, run_count;  // points runs: group blocks
@@ -214,5 +217,36 @@ constexpr int kKeyShift = kTagBits + kLenBits;  // 29
 constexpr uint64_t kLenMask = (uint64_t(1) << kLenBits) - 1;
 constexpr int64_t kPiece = int64_t(1) << kLenBits;  // max granules per piece
 constexpr int kKeyBits = 64 - kKeyShift;            // 35
+
+// ---------------------------------------------------------------- splitting
+// Units whose intervals exceed the shared-memory sort capacity are split by
+// granule-key range: every set measure is additive over disjoint key
+// ranges once intervals are clipped at the boundaries.  The run table is
+// copied into a descriptor in a global arena; ranges are queued for any CTA.
+constexpr int kMaxSubC = 72;
+struct SplitHdr {
+  int64_t cfg;
+  int32_t field, kind, j, n_sub, nr, n_uw;
+  int64_t g, R, kbase, span;
+  int64_t tpb;
+  uint32_t sub_mask[kMaxSubC];
+  int64_t sub_r[kMaxSubC];
+  int32_t sub_sh[kMaxSubC];
+  unsigned long long acc[kMaxSubC];
+  int32_t outstanding;
+  int32_t status;
+};
+struct RangeItem {
+  int64_t desc;  // byte offset of the SplitHdr in the arena
+  int64_t a, b;  // relative key range [a, b)
+  int32_t ready;
+  int32_t pad;
+};
+struct SplitState {
+  unsigned long long qhead, qtail, pending, arena_top;
+  int64_t q_cap, arena_bytes;
+  RangeItem* queue;
+  uint8_t* arena;
+};
 
 }  // namespace gvo

@@ -7,7 +7,7 @@
 namespace gvo {
 
 // dynamic shared memory of the set kernel (2 CTAs per SM)
-constexpr int kSetsSmemBytes = 112 * 1024;
+constexpr int kSetsSmemBytes = 110 * 1024;
 
 void launch_setup(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs,
                   int64_t n, const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos, int64_t* d_ctabs,
@@ -48,6 +48,8 @@ struct SetsLaunch {
   unsigned long long* work = nullptr;
   WarpArgs warp{};
   int64_t n_warp_items = 0;
+  SplitState* split = nullptr;
+  int64_t sm_cap = 0;
 };
 int64_t sets_ebuf_bytes();
 void launch_sets(const SetsLaunch& L, cudaStream_t st);

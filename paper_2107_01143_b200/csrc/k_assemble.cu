@@ -226,16 +226,10 @@ __device__ void assemble_one(const gvo_machine& m, int F, const double* st, int6
 }
 
 // counts -> header, stats, record
-__global__ void k_finish(TplView T, const gvo_machine* machines, const gvo_config* cfgs,
-                         const Geo* geos, int64_t n, int S_req, int W_req, int F,
-                         int64_t* counts, int64_t stride, double* stats, double* records,
-                         double* field_down) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  const Geo& G = geos[c];
-  const gvo_config cfg = cfgs[c];
+__device__ void finish_one(const TplView& T, const gvo_machine* machines, const gvo_config& cfg, const Geo& G,
+                           int64_t c, int S_req, int W_req, int F, int64_t* row, double* stats, double* records,
+                           double* field_down) {
   const gvo_machine m = machines[cfg.machine_id];
-  int64_t* row = counts + c * stride;
   const int64_t sets_status = row[GVO_C_STATUS];
   int status = G.status != GVO_OK ? G.status : (int)sets_status;
   row[GVO_C_STATUS] = status;
@@ -346,6 +340,35 @@ __global__ void k_finish(TplView T, const gvo_machine* machines, const gvo_confi
   }
 }
 
+// warp per config: stage the counts row and the plan in shared memory
+// (coalesced), lane 0 runs the sequential float code from shared memory,
+// the warp writes the resolved row back
+constexpr int kFinishWarps = 4;
+__global__ void __launch_bounds__(32 * kFinishWarps) k_finish(TplView T, const gvo_machine* machines,
+                                                               const gvo_config* cfgs, const Geo* geos, int64_t n,
+                                                               int S_req, int W_req, int F, int64_t* counts,
+                                                               int64_t stride, double* stats, double* records,
+                                                               double* field_down) {
+  extern __shared__ int64_t fsh[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c = (int64_t)blockIdx.x * kFinishWarps + warp;
+  if (c >= n) return;
+  const int64_t geo_words = (sizeof(Geo) + 7) / 8;
+  int64_t* srow = fsh + warp * (stride + geo_words);
+  Geo* sG = reinterpret_cast<Geo*>(srow + stride);
+  int64_t* grow = counts + c * stride;
+  for (int64_t i = lane; i < stride; i += 32) srow[i] = grow[i];
+  const int64_t* gg = reinterpret_cast<const int64_t*>(geos + c);
+  for (int64_t i = lane; i < (int64_t)(sizeof(Geo) / 8); i += 32) reinterpret_cast<int64_t*>(sG)[i] = gg[i];
+  __syncwarp();
+  if (lane == 0) {
+    const gvo_config cfg = cfgs[c];
+    finish_one(T, machines, cfg, *sG, c, S_req, W_req, F, srow, stats, records, field_down);
+  }
+  __syncwarp();
+  for (int64_t i = lane; i < stride; i += 32) grow[i] = srow[i];
+}
+
 // injected float stats (uniform stride F) -> record
 __global__ void k_assemble_stats(const gvo_machine* machines, const int32_t* mid, const int64_t* flops,
                                  int64_t n, int F, const double* stats, double* records,
@@ -365,10 +388,10 @@ void launch_finish(const TplView& T, const gvo_machine* d_machines, const gvo_co
                    int64_t counts_stride, double* d_stats, double* d_records, double* d_field_down,
                    cudaStream_t st) {
   if (n <= 0) return;
-  const int tb = 64;
-  k_finish<<<(unsigned)((n + tb - 1) / tb), tb, 0, st>>>(T, d_machines, d_cfgs, d_geos, n, S_req, W_req, F,
-                                                          d_counts, counts_stride, d_stats, d_records,
-                                                          d_field_down);
+  const size_t smem = kFinishWarps * (counts_stride + (sizeof(Geo) + 7) / 8) * sizeof(int64_t);
+  k_finish<<<(unsigned)((n + kFinishWarps - 1) / kFinishWarps), 32 * kFinishWarps, smem, st>>>(
+      T, d_machines, d_cfgs, d_geos, n, S_req, W_req, F, d_counts, counts_stride, d_stats, d_records,
+      d_field_down);
 }
 
 void launch_assemble_stats(const gvo_machine* d_machines, const int32_t* d_mid, const int64_t* d_flops,

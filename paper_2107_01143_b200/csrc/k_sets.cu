@@ -145,6 +145,17 @@ __device__ inline void emit_lattice(const RunSink& S, Lat L, int tag, const Gran
   r.access = -1;
   r.pieces = pieces;
   r.count = count * pieces;
+  // monotone: with dim 0 fastest, every dim's stride exceeds the span plus
+  // the reach of all faster dims -> bases and interval ends increase with k
+  {
+    bool mono = pieces == 1;
+    unsigned __int128 reach = (unsigned __int128)L.span;
+    for (int d = 0; d < L.nd && mono; ++d) {
+      if (d > 0 && (unsigned __int128)L.st[d] <= reach) mono = false;
+      reach += (unsigned __int128)L.st[d] * (uint64_t)(L.ex[d] - 1);
+    }
+    r.mono = mono ? 1 : 0;
+  }
   r.run_start = r.run_count = 0;
   S.runs[slot] = r;
   atomicMin((long long*)S.key_lo, (long long)G.of(L.base));
@@ -290,6 +301,73 @@ __device__ inline Lat box_lattice(const int64_t* c, const int32_t bd[3], const B
   L.base = (int64_t)base;
   normalize(L, G.g);
   return L;
+}
+
+
+// ------------------------------------------------------------------ decode
+// tuple k of a lattice run -> base address (dim 0 fastest)
+__device__ __forceinline__ uint64_t run_base(const Run& r, int64_t k) {
+  uint64_t b = (uint64_t)r.base;
+  if (k < (int64_t(1) << 31)) {
+    uint32_t k32 = (uint32_t)k;
+    for (int d = 0; d < r.nd; ++d) {
+      const uint32_t ex = (uint32_t)r.ext[d];
+      const uint32_t q = k32 / ex;
+      b += (uint64_t)r.stride[d] * (uint64_t)(k32 - q * ex);
+      k32 = q;
+    }
+  } else {
+    for (int d = 0; d < r.nd; ++d) {
+      const int64_t idx = k % r.ext[d];
+      k /= r.ext[d];
+      b += (uint64_t)r.stride[d] * (uint64_t)idx;
+    }
+  }
+  return b;
+}
+
+// element k of any run -> absolute granule interval [glo, ghi]
+__device__ __forceinline__ void run_interval(const Run& r, int64_t k, const Granule& Gr, const TplView& T, int abase,
+                                             const int64_t* fbase, const int32_t bd[3], const int64_t gd[3],
+                                             int64_t tpb, int64_t* glo, int64_t* ghi) {
+  if (r.kind == 0) {
+    int64_t piece = 0;
+    if (r.pieces > 1) { piece = k % r.pieces; k /= r.pieces; }
+    const uint64_t b = run_base(r, k);
+    int64_t lo = Gr.of((int64_t)b), hi = Gr.of((int64_t)(b + r.span));
+    if (r.pieces > 1) {
+      int64_t plo = lo + piece * kPiece;
+      if (plo > hi) plo = lo;
+      hi = min(hi, plo + kPiece - 1);
+      lo = plo;
+    }
+    *glo = lo;
+    *ghi = hi;
+  } else {
+    const int64_t blk = r.run_start + k / tpb;
+    const int64_t th = k % tpb;
+    int64_t crd[6];
+    crd[0] = th % bd[0];
+    crd[1] = (th / bd[0]) % bd[1];
+    crd[2] = th / ((int64_t)bd[0] * bd[1]);
+    crd[3] = blk % gd[0];
+    crd[4] = (blk / gd[0]) % gd[1];
+    crd[5] = blk / (gd[0] * gd[1]);
+    const int ga = abase + r.access;
+    *glo = *ghi = Gr.of(eval_point(T.code + T.code_off[ga], T.code_len[ga], crd, bd, fbase));
+  }
+}
+
+// first tuple k of a monotone run with (hi ? interval end : start) >= v
+__device__ inline int64_t mono_first(const Run& r, const Granule& Gr, int64_t kbase, int64_t v, bool hi) {
+  int64_t lo = 0, up = r.count;  // pieces == 1 for monotone runs
+  while (lo < up) {
+    const int64_t mid = (lo + up) >> 1;
+    const uint64_t b = run_base(r, mid);
+    const int64_t x = Gr.of((int64_t)(hi ? b + r.span : b)) - kbase;
+    if (x >= v) up = mid; else lo = mid + 1;
+  }
+  return lo;
 }
 
 // ------------------------------------------------------------------ sort
@@ -493,7 +571,49 @@ struct SetsArgs {
   unsigned long long* work; // dynamic work counter (zeroed before launch)
   WarpArgs warp;            // fused warp-statistics items (appended after the set units)
   int64_t n_warp_items;
+  SplitState* split;        // key-range splitting of oversized units (may be null)
+  int64_t sm_cap;           // test hook: cap on shared-memory elements (0 = none)
+  int32_t epoch;            // launch number; queue slots are ready when ready == epoch
 };
+
+// Write a finished unit's measures (union counts per subset) to the outputs.
+__device__ void write_unit_outputs(const SetsArgs& P, int64_t c, int field, int kind, int j, int n_uw,
+                                   const unsigned long long* v /* [n_sub] */) {
+  const int f = field;
+  if (P.mode == 0) {
+    int64_t* row = P.counts + c * P.counts_stride;
+    if (kind == 0) {
+      int64_t* b = row + GVO_C_HDR + ((int64_t)j * P.F_stride + f) * 5;
+      b[0] = (int64_t)v[0];
+      b[2] = (int64_t)v[1];
+      b[3] = (int64_t)v[2];
+    } else {
+      int64_t* wv = row + GVO_C_HDR + (int64_t)P.S_req * P.F_stride * 5;
+      for (int u = 0; u < n_uw; ++u) {
+        int64_t* o = wv + ((int64_t)u * P.F_stride + f) * 4;
+        o[0] = (int64_t)v[4 * u + 0];
+        o[1] = (int64_t)v[4 * u + 1];
+        o[2] = (int64_t)v[4 * u + 2];
+        o[3] = u ? (int64_t)(v[4 * u] + v[4 * (u - 1)] - v[4 * u + 3]) : 0;
+      }
+    }
+  } else if (P.mode == 1) {
+    for (int u = 0; u < n_uw; ++u) {
+      int64_t* o = P.counts + ((int64_t)u * P.F_stride + f) * 4;
+      o[0] = (int64_t)v[4 * u + 0];
+      o[1] = (int64_t)v[4 * u + 1];
+      o[2] = (int64_t)v[4 * u + 2];
+      o[3] = u ? (int64_t)(v[4 * u] + v[4 * (u - 1)] - v[4 * u + 3]) : 0;
+    }
+  } else {
+    P.counts[f * 2 + 0] = (int64_t)v[0];
+    P.counts[f * 2 + 1] = (int64_t)v[1];
+  }
+}
+
+__device__ __forceinline__ unsigned long long vload(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
 
 __global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -504,378 +624,674 @@ __global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
   int64_t* wmax = reinterpret_cast<int64_t*>(smem + off); off += kMaxSub * kNW * 8;
   int64_t* roff_sh = reinterpret_cast<int64_t*>(smem + off); off += (kSmemRuns + 1) * 8;
   int64_t* cpts = reinterpret_cast<int64_t*>(smem + off); off += kNW * kClassPts * 8;
+  int64_t* rka_sh = reinterpret_cast<int64_t*>(smem + off); off += kSmemRuns * 8;
   uint64_t* ebuf = reinterpret_cast<uint64_t*>(smem + off);
-  const int64_t sm_elems = (int64_t)(kSetsSmemBytes - off) / 16;
+  const int64_t sm_elems = P.sm_cap > 0 ? min((int64_t)(kSetsSmemBytes - off) / 16, P.sm_cap)
+                                         : (int64_t)(kSetsSmemBytes - off) / 16;
 
   uint8_t* slab = P.slab + (int64_t)blockIdx.x * P.slab_bytes;
   Run* runs = reinterpret_cast<Run*>(slab);
   int64_t* roff_gl = reinterpret_cast<int64_t*>(slab + P.run_cap * sizeof(Run));
-  uint64_t* gbuf = reinterpret_cast<uint64_t*>(slab + P.run_cap * sizeof(Run) + (P.run_cap + 1) * 8);
+  int64_t* rka_gl = roff_gl + (P.run_cap + 1);
+  uint64_t* gbuf = reinterpret_cast<uint64_t*>(slab + P.run_cap * sizeof(Run) + 2 * (P.run_cap + 1) * 8);
+  SplitState* SS = P.split;
 
   __shared__ int64_t next_item;
+  __shared__ int next_kind;  // 0 main item, 1 range item, 2 exit
+  __shared__ RangeItem cur_range;
+  __shared__ int main_done;
+  if (threadIdx.x == 0) main_done = 0;
+  const int64_t n_main = P.n_items + P.n_warp_items;
+
   for (;;) {
-    // dynamic fetch: wave units (the heavy ones) are numbered first
-    if (threadIdx.x == 0) next_item = (int64_t)atomicAdd(P.work, 1ull);
+    // ---------------- fetch: queued key ranges first, then main items
+    if (threadIdx.x == 0) {
+      int kind = 2;
+      int64_t it = -1;
+      for (;;) {
+        if (SS) {
+          const unsigned long long t = min(vload(&SS->qtail), (unsigned long long)SS->q_cap);
+          const unsigned long long h = vload(&SS->qhead);
+          if (h < t) {
+            if (atomicCAS(&SS->qhead, h, h + 1) == h) {
+              volatile int32_t* rd = &SS->queue[h].ready;
+              while (*rd != P.epoch) __nanosleep(64);
+              __threadfence();
+              cur_range = SS->queue[h];
+              kind = 1;
+              break;
+            }
+            continue;
+          }
+        }
+        if (!main_done) {
+          const unsigned long long m = atomicAdd(P.work, 1ull);
+          if ((int64_t)m < n_main) {
+            kind = 0;
+            it = (int64_t)m;
+            if (SS) atomicAdd(&SS->pending, 1ull);
+            break;
+          }
+          main_done = 1;
+        }
+        if (!SS || (vload(&SS->pending) == 0 && vload(&SS->qhead) >= min(vload(&SS->qtail), (unsigned long long)SS->q_cap)))
+          break;
+        __nanosleep(256);
+      }
+      next_kind = kind;
+      next_item = it;
+    }
     __syncthreads();
+    const int kind_fetched = next_kind;
     const int64_t item = next_item;
-    if (item >= P.n_items + P.n_warp_items) break;
-    if (item >= P.n_items) {
+    if (kind_fetched == 2) break;
+
+    int64_t range_a = 0, range_b = 0;
+    SplitHdr* hdr = nullptr;
+    bool in_range = kind_fetched == 1;
+    const long long t_start = clock64();
+
+    if (!in_range && item >= P.n_items) {
       warp_item(P.warp, item - P.n_items, reinterpret_cast<unsigned long long*>(ebuf));
       __syncthreads();
+      if (threadIdx.x == 0 && SS) atomicAdd(&SS->pending, ~0ull);
       continue;
     }
-    const long long t_start = clock64();
+
+    if (!in_range) {
     // ---------------- unit description
-    if (threadIdx.x == 0) {
-      U.status = GVO_OK;
-      U.n_runs = 0;
-      U.key_lo = INT64_MAX;
-      U.key_hi = INT64_MIN;
-      U.n_src = 0;
-      U.n_sub = 0;
-      int64_t c, f;
-      int j = 0;
-      bool skip = false;
-      if (P.mode == 0) {
-        const int64_t n_cfg = P.n_items / ((int64_t)P.F_stride * (P.S_req + 1));
-        const int64_t n_wave = n_cfg * P.F_stride;
-        if (item < n_wave) {
-          c = item / P.F_stride;
-          f = item % P.F_stride;
-          j = P.S_req;
-        } else {
-          const int64_t r = item - n_wave;
-          c = r / ((int64_t)P.F_stride * P.S_req);
-          f = (r / P.S_req) % P.F_stride;
-          j = (int)(r % P.S_req);
-        }
-      } else {
-        c = 0;
-        f = item;
-      }
-      const Geo& G = P.geos[c];
-      const gvo_config& cfg = P.cfgs[c];
-      if (f >= P.T.n_fields[cfg.template_id]) skip = true;
-      if (P.mode == 0 && !phase_ok(G, j < P.S_req ? 0 : 1)) skip = true;
-      U.cfg = c;
-      U.field = (int)f;
-      U.j = j;
-      if (!skip && P.mode == 0 && j < P.S_req) {
-        if (j >= G.n_samples || G.dup_of[f][j] >= 0) skip = true;
-        else {
-          U.kind = 0;
-          U.n_src = 2;
-          for (int k = 0; k < 2; ++k) {
-            U.src_start[k] = G.sample_lin[j];
-            U.src_count[k] = 1;
-            U.src_kind[k] = k;
-            U.src_tag[k] = k;
-          }
-          U.n_sub = 3;
-          U.sub_mask[0] = 1; U.sub_r[0] = 1;            // load sectors
-          U.sub_mask[1] = 1; U.sub_r[1] = 1;            // load lines (r set below)
-          U.sub_mask[2] = 2; U.sub_r[2] = 1;            // store sectors
-        }
-      } else if (!skip && P.mode != 2) {
-        U.kind = 1;
-        U.n_src = 2 * G.n_uw;
-        for (int u = 0; u < G.n_uw; ++u)
-          for (int k = 0; k < 2; ++k) {
-            U.src_start[2 * u + k] = G.uw_start[u];
-            U.src_count[2 * u + k] = G.uw_count[u];
-            U.src_kind[2 * u + k] = k;
-            U.src_tag[2 * u + k] = 2 * u + k;
-          }
-        int q = 0;
-        for (int u = 0; u < G.n_uw; ++u) {
-          U.sub_mask[q] = 1u << (2 * u); U.sub_r[q++] = 1;
-          U.sub_mask[q] = 1u << (2 * u + 1); U.sub_r[q++] = 1;
-          U.sub_mask[q] = 3u << (2 * u); U.sub_r[q++] = 1;
-          U.sub_mask[q] = u ? (1u << (2 * u)) | (1u << (2 * u - 2)) : 0u; U.sub_r[q++] = 1;
-        }
-        U.n_sub = q;
-      } else if (!skip) {
-        U.kind = 2;
-        U.n_src = 0;
-        if (2 * P.n_custom_runs > kMaxSrc) { skip = true; atomicExch(P.status_out, GVO_ERR_UNSUPPORTED); }
-        for (int r = 0; r < P.n_custom_runs && U.n_src + 2 <= kMaxSrc; ++r)
-          for (int k = 0; k < 2; ++k) {
-            U.src_start[U.n_src] = P.run_start[r];
-            U.src_count[U.n_src] = P.run_count[r];
-            U.src_kind[U.n_src] = k;
-            U.src_tag[U.n_src] = k;
-            ++U.n_src;
-          }
-        U.n_sub = 2;
-        U.sub_mask[0] = 1; U.sub_r[0] = 1;
-        U.sub_mask[1] = 2; U.sub_r[1] = 1;
-      }
-      if (skip) U.n_src = -1;
-    }
-    __syncthreads();
-    if (U.n_src < 0) { __syncthreads(); continue; }
-
-    const int64_t c = U.cfg;
-    const Geo& G = P.geos[c];
-    const gvo_config cfg = P.cfgs[c];
-    const int tpl = cfg.template_id;
-    const int abase = P.T.acc_base[tpl];
-    const int64_t* fbase = P.T.field_base + P.T.field_base_off[tpl];
-    const int32_t bd[3] = {cfg.block[0], cfg.block[1], cfg.block[2]};
-    const int64_t gd[3] = {cfg.grid[0], cfg.grid[1], cfg.grid[2]};
-    const int64_t* crow = P.coefs + c * (int64_t)P.T.max_acc * 8;
-    const gvo_machine& mach = P.machines[cfg.machine_id];
-    const int64_t g = P.mode == 0 ? mach.sector_bytes : P.granularity;
-    const Granule Gr = Granule::make(g);
-    const int64_t R = P.mode == 0 ? mach.l1_line_bytes / mach.sector_bytes : 1;
-    if (threadIdx.x == 0) {
-      U.g = g;
-      U.R = R;
-      if (U.kind == 0) U.sub_r[1] = R;
-      for (int q = 0; q < U.n_sub; ++q) {
-        const int64_t r = U.sub_r[q];
-        int sh = -1;
-        if (r > 0 && (r & (r - 1)) == 0) { sh = 0; while ((int64_t(1) << sh) < r) ++sh; }
-        U.sub_sh[q] = sh;
-      }
-    }
-    const int64_t tpb = G.tpb;
-    RunSink sink{runs, (int)P.run_cap, &U.n_runs, &U.status, &U.key_lo, &U.key_hi};
-    __syncthreads();
-
-    // ---------------- run building
-    // (a) points runs for non-affine accesses: one task per (source, access)
-    const int32_t* fko = P.T.fk_off + tpl * (2 * kMaxFields + 1);
-    for (int task = threadIdx.x; task < U.n_src * 64; task += kNT) {
-      const int s = task >> 6;
-      const int slot = U.field * 2 + U.src_kind[s];
-      const int fk = fko[slot], na = fko[slot + 1] - fk;
-      for (int q = task & 63; q < na; q += 64) {
-        const int a = P.T.fk_list[fk + q];
-        if (crow[a * 8 + 7] == kAffine) continue;
-        int64_t clo[6], chi[6];
-        clo[0] = clo[1] = clo[2] = 0;
-        chi[0] = bd[0] - 1; chi[1] = bd[1] - 1; chi[2] = bd[2] - 1;
-        run_bid_bounds(U.src_start[s], U.src_count[s], gd, clo + 3, chi + 3);
-        int64_t lo, hi;
-        const int ga = abase + a;
-        bounds_check(P.T.code + P.T.code_off[ga], P.T.code_len[ga], clo, chi, bd, fbase, &lo, &hi);
-        const int slot_r = atomicAdd(&U.n_runs, 1);
-        if (slot_r >= P.run_cap) { atomicExch(&U.status, GVO_ERR_CAPACITY); continue; }
-        Run r;
-        r.kind = 1;
-        r.access = a;
-        r.tag = U.src_tag[s];
-        r.run_start = U.src_start[s];
-        r.run_count = U.src_count[s];
-        r.count = U.src_count[s] * tpb;
-        r.pieces = 1;
-        r.nd = 0;
-        r.base = 0;
-        r.span = 0;
-        runs[slot_r] = r;
-        atomicMin((long long*)&U.key_lo, (long long)Gr.of(lo));
-        atomicMax((long long*)&U.key_hi, (long long)Gr.of(hi));
-      }
-    }
-    // (b) lattices: one WARP per (source, box, coefficient class)
-    {
-      const CTab ct{const_cast<int64_t*>(P.ctabs) + c * ctab_stride(P.T.max_acc), P.T.max_acc};
-      const int slot0 = U.field * 2;
-      const int ncl0 = (int)(ct.slot_first()[slot0 + 1] - ct.slot_first()[slot0]);
-      const int ncl1 = (int)(ct.slot_first()[slot0 + 2] - ct.slot_first()[slot0 + 1]);
-      const int ncl = max(ncl0, ncl1);
-      const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-      int64_t* wpts = cpts + wid * kClassPts;
-      for (int task = wid; task < U.n_src * 5 * ncl; task += kNW) {
-        const int s = task / (5 * ncl), rem = task % (5 * ncl), bi = rem / ncl, ci = rem % ncl;
-        const int slot = slot0 + U.src_kind[s];
-        const int64_t cl0 = ct.slot_first()[slot];
-        if (ci >= ct.slot_first()[slot + 1] - cl0) continue;
-        Box boxes[5];
-        const int nb = run_boxes(U.src_start[s], U.src_count[s], gd, boxes);
-        if (bi >= nb) continue;
-        const int64_t cls = cl0 + ci;
-        const int64_t* ca = crow + ct.rep()[cls] * 8;
-        const Lat L0 = box_lattice(ca, bd, boxes[bi], Gr);
-        const int64_t* cp = ct.pts() + ct.start()[cls];
-        const int64_t np = ct.cnt()[cls];
-        for (int64_t p0 = 0; p0 < np; p0 += kClassPts) {
-          const int m = (int)((np - p0) < kClassPts ? (np - p0) : kClassPts);
-          __syncwarp();
-          for (int k = lane; k < m; k += 32) wpts[k] = (int64_t)((uint64_t)L0.base + (uint64_t)cp[p0 + k]);
-          __syncwarp();
-          cover_warp(sink, L0, wpts, m, U.src_tag[s], Gr);
-        }
-      }
-    }
-    __syncthreads();
-
-    const long long t_runs = clock64();
-    // ---------------- offsets of runs, element count
-    const int nr = min(U.n_runs, (int)P.run_cap);
-    int64_t* roff = nr <= kSmemRuns ? roff_sh : roff_gl;
-    if (threadIdx.x == 0) {
-      int64_t acc = 0;
-      for (int r = 0; r < nr; ++r) { roff[r] = acc; acc += runs[r].count; }
-      roff[nr] = acc;
-      U.N = acc;
-      const int64_t base = floordiv(U.key_lo, U.R) * U.R;
-      U.key_lo = base;
-      if (U.status == GVO_OK) {
-        if (nr > 0 && (uint64_t)(U.key_hi - base) >= (uint64_t(1) << kKeyBits)) U.status = GVO_ERR_UNSUPPORTED;
-        if (acc > P.elem_cap) U.status = GVO_ERR_CAPACITY;
-      }
-    }
-    __syncthreads();
-    if (U.status != GVO_OK) {
       if (threadIdx.x == 0) {
+        U.status = GVO_OK;
+        U.n_runs = 0;
+        U.key_lo = INT64_MAX;
+        U.key_hi = INT64_MIN;
+        U.n_src = 0;
+        U.n_sub = 0;
+        int64_t c, f;
+        int j = 0;
+        bool skip = false;
         if (P.mode == 0) {
-          int64_t* row = P.counts + c * P.counts_stride;
-          atomicExch((unsigned long long*)&row[GVO_C_STATUS], (unsigned long long)U.status);
+          const int64_t n_cfg = P.n_items / ((int64_t)P.F_stride * (P.S_req + 1));
+          const int64_t n_wave = n_cfg * P.F_stride;
+          if (item < n_wave) {
+            c = item / P.F_stride;
+            f = item % P.F_stride;
+            j = P.S_req;
+          } else {
+            const int64_t r = item - n_wave;
+            c = r / ((int64_t)P.F_stride * P.S_req);
+            f = (r / P.S_req) % P.F_stride;
+            j = (int)(r % P.S_req);
+          }
         } else {
-          atomicExch(P.status_out, U.status);
+          c = 0;
+          f = item;
         }
+        const Geo& G = P.geos[c];
+        const gvo_config& cfg = P.cfgs[c];
+        if (f >= P.T.n_fields[cfg.template_id]) skip = true;
+        if (P.mode == 0 && !phase_ok(G, j < P.S_req ? 0 : 1)) skip = true;
+        U.cfg = c;
+        U.field = (int)f;
+        U.j = j;
+        if (!skip && P.mode == 0 && j < P.S_req) {
+          if (j >= G.n_samples || G.dup_of[f][j] >= 0) skip = true;
+          else {
+            U.kind = 0;
+            U.n_src = 2;
+            for (int k = 0; k < 2; ++k) {
+              U.src_start[k] = G.sample_lin[j];
+              U.src_count[k] = 1;
+              U.src_kind[k] = k;
+              U.src_tag[k] = k;
+            }
+            U.n_sub = 3;
+            U.sub_mask[0] = 1; U.sub_r[0] = 1;            // load sectors
+            U.sub_mask[1] = 1; U.sub_r[1] = 1;            // load lines (r set below)
+            U.sub_mask[2] = 2; U.sub_r[2] = 1;            // store sectors
+          }
+        } else if (!skip && P.mode != 2) {
+          U.kind = 1;
+          U.n_src = 2 * G.n_uw;
+          for (int u = 0; u < G.n_uw; ++u)
+            for (int k = 0; k < 2; ++k) {
+              U.src_start[2 * u + k] = G.uw_start[u];
+              U.src_count[2 * u + k] = G.uw_count[u];
+              U.src_kind[2 * u + k] = k;
+              U.src_tag[2 * u + k] = 2 * u + k;
+            }
+          int q = 0;
+          for (int u = 0; u < G.n_uw; ++u) {
+            U.sub_mask[q] = 1u << (2 * u); U.sub_r[q++] = 1;
+            U.sub_mask[q] = 1u << (2 * u + 1); U.sub_r[q++] = 1;
+            U.sub_mask[q] = 3u << (2 * u); U.sub_r[q++] = 1;
+            U.sub_mask[q] = u ? (1u << (2 * u)) | (1u << (2 * u - 2)) : 0u; U.sub_r[q++] = 1;
+          }
+          U.n_sub = q;
+        } else if (!skip) {
+          U.kind = 2;
+          U.n_src = 0;
+          if (2 * P.n_custom_runs > kMaxSrc) { skip = true; atomicExch(P.status_out, GVO_ERR_UNSUPPORTED); }
+          for (int r = 0; r < P.n_custom_runs && U.n_src + 2 <= kMaxSrc; ++r)
+            for (int k = 0; k < 2; ++k) {
+              U.src_start[U.n_src] = P.run_start[r];
+              U.src_count[U.n_src] = P.run_count[r];
+              U.src_kind[U.n_src] = k;
+              U.src_tag[U.n_src] = k;
+              ++U.n_src;
+            }
+          U.n_sub = 2;
+          U.sub_mask[0] = 1; U.sub_r[0] = 1;
+          U.sub_mask[1] = 2; U.sub_r[1] = 1;
+        }
+        if (skip) U.n_src = -1;
+      }
+      __syncthreads();
+      __syncthreads();
+      if (U.n_src < 0) {
+        if (threadIdx.x == 0 && SS) atomicAdd(&SS->pending, ~0ull);
+        __syncthreads();
+        continue;
+      }
+    }
+
+    // ---------------- main unit: run building, element count
+    if (!in_range) {
+    const int64_t c = U.cfg;
+      const Geo& G = P.geos[c];
+      const gvo_config cfg = P.cfgs[c];
+      const int tpl = cfg.template_id;
+      const int abase = P.T.acc_base[tpl];
+      const int64_t* fbase = P.T.field_base + P.T.field_base_off[tpl];
+      const int32_t bd[3] = {cfg.block[0], cfg.block[1], cfg.block[2]};
+      const int64_t gd[3] = {cfg.grid[0], cfg.grid[1], cfg.grid[2]};
+      const int64_t* crow = P.coefs + c * (int64_t)P.T.max_acc * 8;
+      const gvo_machine& mach = P.machines[cfg.machine_id];
+      const int64_t g = P.mode == 0 ? mach.sector_bytes : P.granularity;
+      const Granule Gr = Granule::make(g);
+      const int64_t R = P.mode == 0 ? mach.l1_line_bytes / mach.sector_bytes : 1;
+      if (threadIdx.x == 0) {
+        U.g = g;
+        U.R = R;
+        if (U.kind == 0) U.sub_r[1] = R;
+        for (int q = 0; q < U.n_sub; ++q) {
+          const int64_t r = U.sub_r[q];
+          int sh = -1;
+          if (r > 0 && (r & (r - 1)) == 0) { sh = 0; while ((int64_t(1) << sh) < r) ++sh; }
+          U.sub_sh[q] = sh;
+        }
+      }
+      const int64_t tpb = G.tpb;
+      RunSink sink{runs, (int)P.run_cap, &U.n_runs, &U.status, &U.key_lo, &U.key_hi};
+      __syncthreads();
+
+      // ---------------- run building
+      // (a) points runs for non-affine accesses: one task per (source, access)
+      const int32_t* fko = P.T.fk_off + tpl * (2 * kMaxFields + 1);
+      for (int task = threadIdx.x; task < U.n_src * 64; task += kNT) {
+        const int s = task >> 6;
+        const int slot = U.field * 2 + U.src_kind[s];
+        const int fk = fko[slot], na = fko[slot + 1] - fk;
+        for (int q = task & 63; q < na; q += 64) {
+          const int a = P.T.fk_list[fk + q];
+          if (crow[a * 8 + 7] == kAffine) continue;
+          int64_t clo[6], chi[6];
+          clo[0] = clo[1] = clo[2] = 0;
+          chi[0] = bd[0] - 1; chi[1] = bd[1] - 1; chi[2] = bd[2] - 1;
+          run_bid_bounds(U.src_start[s], U.src_count[s], gd, clo + 3, chi + 3);
+          int64_t lo, hi;
+          const int ga = abase + a;
+          bounds_check(P.T.code + P.T.code_off[ga], P.T.code_len[ga], clo, chi, bd, fbase, &lo, &hi);
+          const int slot_r = atomicAdd(&U.n_runs, 1);
+          if (slot_r >= P.run_cap) { atomicExch(&U.status, GVO_ERR_CAPACITY); continue; }
+          Run r;
+          r.kind = 1;
+          r.access = a;
+          r.tag = U.src_tag[s];
+          r.run_start = U.src_start[s];
+          r.run_count = U.src_count[s];
+          r.count = U.src_count[s] * tpb;
+          r.mono = 0;
+          r.pieces = 1;
+          r.nd = 0;
+          r.base = 0;
+          r.span = 0;
+          runs[slot_r] = r;
+          atomicMin((long long*)&U.key_lo, (long long)Gr.of(lo));
+          atomicMax((long long*)&U.key_hi, (long long)Gr.of(hi));
+        }
+      }
+      // (b) lattices: one WARP per (source, box, coefficient class)
+      {
+        const CTab ct{const_cast<int64_t*>(P.ctabs) + c * ctab_stride(P.T.max_acc), P.T.max_acc};
+        const int slot0 = U.field * 2;
+        const int ncl0 = (int)(ct.slot_first()[slot0 + 1] - ct.slot_first()[slot0]);
+        const int ncl1 = (int)(ct.slot_first()[slot0 + 2] - ct.slot_first()[slot0 + 1]);
+        const int ncl = max(ncl0, ncl1);
+        const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        int64_t* wpts = cpts + wid * kClassPts;
+        for (int task = wid; task < U.n_src * 5 * ncl; task += kNW) {
+          const int s = task / (5 * ncl), rem = task % (5 * ncl), bi = rem / ncl, ci = rem % ncl;
+          const int slot = slot0 + U.src_kind[s];
+          const int64_t cl0 = ct.slot_first()[slot];
+          if (ci >= ct.slot_first()[slot + 1] - cl0) continue;
+          Box boxes[5];
+          const int nb = run_boxes(U.src_start[s], U.src_count[s], gd, boxes);
+          if (bi >= nb) continue;
+          const int64_t cls = cl0 + ci;
+          const int64_t* ca = crow + ct.rep()[cls] * 8;
+          const Lat L0 = box_lattice(ca, bd, boxes[bi], Gr);
+          const int64_t* cp = ct.pts() + ct.start()[cls];
+          const int64_t np = ct.cnt()[cls];
+          for (int64_t p0 = 0; p0 < np; p0 += kClassPts) {
+            const int m = (int)((np - p0) < kClassPts ? (np - p0) : kClassPts);
+            __syncwarp();
+            for (int k = lane; k < m; k += 32) wpts[k] = (int64_t)((uint64_t)L0.base + (uint64_t)cp[p0 + k]);
+            __syncwarp();
+            cover_warp(sink, L0, wpts, m, U.src_tag[s], Gr);
+          }
+        }
+      }
+      __syncthreads();
+
+    // ---------------- offsets of runs, element count
+      const int nr = min(U.n_runs, (int)P.run_cap);
+      int64_t* roff = nr <= kSmemRuns ? roff_sh : roff_gl;
+      if (threadIdx.x == 0) {
+        int64_t acc = 0;
+        for (int r = 0; r < nr; ++r) { roff[r] = acc; acc += runs[r].count; }
+        roff[nr] = acc;
+        U.N = acc;
+        const int64_t base = floordiv(U.key_lo, U.R) * U.R;
+        U.key_lo = base;
+        if (U.status == GVO_OK) {
+          if (nr > 0 && (uint64_t)(U.key_hi - base) >= (uint64_t(1) << kKeyBits)) U.status = GVO_ERR_UNSUPPORTED;
+          if (acc > P.elem_cap) U.status = GVO_ERR_CAPACITY;
+        }
+      }
+      __syncthreads();
+      if (U.status != GVO_OK) {
+        if (threadIdx.x == 0) {
+          if (P.mode == 0) {
+            int64_t* row = P.counts + c * P.counts_stride;
+            atomicExch((unsigned long long*)&row[GVO_C_STATUS], (unsigned long long)U.status);
+          } else {
+            atomicExch(P.status_out, U.status);
+          }
+          if (SS) atomicAdd(&SS->pending, ~0ull);
+        }
+        __syncthreads();
+        continue;
+      }
+
+      // too big for shared memory: turn the unit into a split descriptor
+      // and continue as its first key range [0, span]
+      if (U.N > sm_elems && SS) {
+        __shared__ int64_t desc_off;
+        if (threadIdx.x == 0) {
+          const int64_t hb = (sizeof(SplitHdr) + 15) & ~int64_t(15);
+          const int64_t need = hb + (int64_t)nr * (int64_t)sizeof(Run);
+          const unsigned long long o = atomicAdd(&SS->arena_top, (unsigned long long)need);
+          desc_off = (int64_t)(o + need) <= SS->arena_bytes ? (int64_t)o : -1;
+          if (desc_off >= 0) {
+            SplitHdr* h = reinterpret_cast<SplitHdr*>(SS->arena + desc_off);
+            h->cfg = c; h->field = U.field; h->kind = U.kind; h->j = U.j; h->n_sub = U.n_sub; h->nr = nr;
+            h->n_uw = P.mode == 2 ? 0 : G.n_uw;
+            h->g = U.g; h->R = U.R; h->kbase = U.key_lo; h->span = U.key_hi - U.key_lo; h->tpb = G.tpb;
+            for (int q = 0; q < U.n_sub; ++q) {
+              h->sub_mask[q] = U.sub_mask[q]; h->sub_r[q] = U.sub_r[q]; h->sub_sh[q] = U.sub_sh[q]; h->acc[q] = 0ull;
+            }
+            h->outstanding = 1;
+            h->status = GVO_OK;
+          }
+        }
+        __syncthreads();
+        if (desc_off >= 0) {
+          Run* dr = reinterpret_cast<Run*>(SS->arena + desc_off + ((sizeof(SplitHdr) + 15) & ~size_t(15)));
+          for (int r = threadIdx.x; r < nr; r += kNT) dr[r] = runs[r];
+          __threadfence();
+          __syncthreads();
+          hdr = reinterpret_cast<SplitHdr*>(SS->arena + desc_off);
+          in_range = true;
+          range_a = 0;
+          range_b = ((U.key_hi - U.key_lo) / U.R + 1) * U.R;
+        }
+      }
+    } else {
+      if (threadIdx.x == 0) {
+        hdr = reinterpret_cast<SplitHdr*>(SS->arena + cur_range.desc);
+      }
+      range_a = cur_range.a;
+      range_b = cur_range.b;
+      hdr = reinterpret_cast<SplitHdr*>(SS->arena + cur_range.desc);
+      if (threadIdx.x == 0) {
+        U.cfg = hdr->cfg; U.field = hdr->field; U.kind = hdr->kind; U.j = hdr->j; U.n_sub = hdr->n_sub;
+        U.g = hdr->g; U.R = hdr->R; U.key_lo = hdr->kbase;
+        for (int q = 0; q < hdr->n_sub; ++q) {
+          U.sub_mask[q] = hdr->sub_mask[q]; U.sub_r[q] = hdr->sub_r[q]; U.sub_sh[q] = hdr->sub_sh[q];
+        }
+        U.status = GVO_OK;
+      }
+      __syncthreads();
+    }
+
+    if (in_range) {
+      // ================= key-range processing of a split unit =================
+      const int64_t c = hdr->cfg;
+      const gvo_config cfg = P.cfgs[c];
+      const int tpl = cfg.template_id;
+      const int abase = P.T.acc_base[tpl];
+      const int64_t* fbase = P.T.field_base + P.T.field_base_off[tpl];
+      const int32_t bd[3] = {cfg.block[0], cfg.block[1], cfg.block[2]};
+      const int64_t gd[3] = {cfg.grid[0], cfg.grid[1], cfg.grid[2]};
+      const Granule Gr = Granule::make(hdr->g);
+      const int64_t kbase = hdr->kbase, R = hdr->R, tpb = hdr->tpb;
+      const int nr = hdr->nr;
+      const Run* druns = reinterpret_cast<const Run*>(reinterpret_cast<const uint8_t*>(hdr) +
+                                                      ((sizeof(SplitHdr) + 15) & ~size_t(15)));
+      int64_t* rcnt = nr <= kSmemRuns ? roff_sh : roff_gl;
+      int64_t* rka = nr <= kSmemRuns ? rka_sh : rka_gl;
+      __shared__ int64_t s_N;
+      __shared__ int s_split;
+      int64_t a = range_a, b = range_b;
+      for (;;) {
+        // count in-range elements per run (monotone runs: bisection)
+        for (int r = threadIdx.x; r < nr; r += kNT) {
+          const Run& rr = druns[r];
+          if (rr.kind == 0 && rr.mono) {
+            const int64_t ka = mono_first(rr, Gr, kbase, a, true);
+            const int64_t kb = mono_first(rr, Gr, kbase, b, false);
+            rka[r] = ka;
+            rcnt[r] = kb > ka ? kb - ka : 0;
+          } else {
+            rka[r] = -1;
+            rcnt[r] = 0;
+          }
+        }
+        __syncthreads();
+        // non-monotone runs: scan all their elements (rare)
+        for (int r = 0; r < nr; ++r) {
+          if (rka[r] >= 0) continue;
+          const Run& rr = druns[r];
+          int64_t local = 0;
+          for (int64_t k = threadIdx.x; k < rr.count; k += kNT) {
+            int64_t lo, hi;
+            run_interval(rr, k, Gr, P.T, abase, fbase, bd, gd, tpb, &lo, &hi);
+            lo -= kbase; hi -= kbase;
+            local += (lo < b && hi >= a) ? 1 : 0;
+          }
+          for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+          if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = local;
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            int64_t t = 0;
+            for (int w = 0; w < kNW; ++w) t += wmax[w];
+            rcnt[r] = t;
+          }
+          __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+          int64_t acc = 0;
+          for (int r = 0; r < nr; ++r) { const int64_t v = rcnt[r]; rcnt[r] = acc; acc += v; }
+          rcnt[nr] = acc;
+          s_N = acc;
+          s_split = 0;
+          if (acc > sm_elems && b - a > R) {
+            const int64_t mid = a + ((b - a) / (2 * R)) * R;
+            if (mid > a && mid < b) {
+              atomicAdd(&hdr->outstanding, 1);
+              atomicAdd(&SS->pending, 1ull);
+              const unsigned long long slot = atomicAdd(&SS->qtail, 1ull);
+              if ((int64_t)slot < SS->q_cap) {
+                RangeItem it;
+                it.desc = (int64_t)(reinterpret_cast<uint8_t*>(hdr) - SS->arena);
+                it.a = mid;
+                it.b = b;
+                it.ready = 0;
+                it.pad = 0;
+                SS->queue[slot] = it;
+                __threadfence();
+                *reinterpret_cast<volatile int32_t*>(&SS->queue[slot].ready) = P.epoch;
+                s_split = 1;
+                b = mid;
+              } else {
+                atomicSub(&hdr->outstanding, 1);
+                atomicAdd(&SS->pending, ~0ull);
+              }
+            }
+          }
+          cur_range.a = a;
+          cur_range.b = b;
+        }
+        __syncthreads();
+        b = cur_range.b;
+        if (!s_split) break;
+      }
+      const int64_t N = s_N;
+      if (N > P.elem_cap) {
+        if (threadIdx.x == 0) atomicExch(&hdr->status, GVO_ERR_CAPACITY);
+      } else {
+        uint64_t* A0 = N <= sm_elems ? ebuf : gbuf;
+        uint64_t* B0 = N <= sm_elems ? ebuf + sm_elems : gbuf + P.elem_cap;
+        // emission (clipped to [a, b), keys relative to a)
+        {
+          const int64_t per = (N + kNT - 1) / kNT;
+          const int64_t e0 = min(N, (int64_t)threadIdx.x * per), e1 = min(N, e0 + per);
+          int ri = 0;
+          if (e0 < e1) {
+            int lo = 0, hi = nr - 1;
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (rcnt[mid] <= e0) lo = mid; else hi = mid - 1;
+            }
+            ri = lo;
+          }
+          for (int64_t i = e0; i < e1; ++i) {
+            while (rcnt[ri + 1] <= i) ++ri;
+            if (rka[ri] < 0) continue;  // non-monotone runs: compacted below
+            const Run& rr = druns[ri];
+            const int64_t k = rka[ri] + (i - rcnt[ri]);
+            int64_t lo, hi;
+            run_interval(rr, k, Gr, P.T, abase, fbase, bd, gd, tpb, &lo, &hi);
+            lo = max(lo - kbase, a);
+            hi = min(hi - kbase, b - 1);
+            A0[i] = ((uint64_t)(lo - a) << kKeyShift) | ((uint64_t)(hi - lo) << kTagBits) | (uint64_t)rr.tag;
+          }
+        }
+        __shared__ unsigned long long fillc;
+        for (int r = 0; r < nr; ++r) {
+          if (rka[r] >= 0) continue;
+          if (threadIdx.x == 0) fillc = 0;
+          __syncthreads();
+          const Run& rr = druns[r];
+          for (int64_t k = threadIdx.x; k < rr.count; k += kNT) {
+            int64_t lo, hi;
+            run_interval(rr, k, Gr, P.T, abase, fbase, bd, gd, tpb, &lo, &hi);
+            lo -= kbase; hi -= kbase;
+            if (lo < b && hi >= a) {
+              lo = max(lo, a);
+              hi = min(hi, b - 1);
+              const unsigned long long slot = atomicAdd(&fillc, 1ull);
+              A0[rcnt[r] + (int64_t)slot] = ((uint64_t)(lo - a) << kKeyShift) | ((uint64_t)(hi - lo) << kTagBits) |
+                                            (uint64_t)rr.tag;
+            }
+          }
+          __syncthreads();
+        }
+        __syncthreads();
+        int kb = 0;
+        {
+          uint64_t span = (uint64_t)(b - a - 1);
+          while (span) { ++kb; span >>= 1; }
+        }
+        const uint64_t* sorted = cta_sort(A0, B0, N, kKeyShift, ((kb + 7) / 8) * 8, hist, tot);
+        sweep(sorted, N, U, wmax);
+        if (threadIdx.x < U.n_sub) atomicAdd(&hdr->acc[threadIdx.x], (unsigned long long)U.sub_val[threadIdx.x]);
+      }
+      if (threadIdx.x == 0 && P.unit_stats) {
+        // range statistics after the unit slots: [idx][10]
+        const unsigned long long ri = atomicAdd(&SS->arena_top, 0ull);  // keep ordering cheap
+        (void)ri;
+        const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(P.unit_stats + P.n_items * 10), 1ull);
+        if (slot < 4096) {
+          int64_t* us = P.unit_stats + P.n_items * 10 + 10 + slot * 10;
+          us[0] = (int64_t)(reinterpret_cast<uint8_t*>(hdr) - SS->arena);
+          us[1] = a; us[2] = b; us[3] = N; us[4] = clock64() - t_start; us[5] = nr;
+          unsigned smid;
+          asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+          us[6] = smid; us[7] = hdr->cfg; us[8] = kind_fetched;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicSub(&hdr->outstanding, 1) == 1) {
+          __threadfence();
+          if (hdr->status != GVO_OK) {
+            if (P.mode == 0) {
+              int64_t* row = P.counts + c * P.counts_stride;
+              atomicExch((unsigned long long*)&row[GVO_C_STATUS], (unsigned long long)hdr->status);
+            } else {
+              atomicExch(P.status_out, hdr->status);
+            }
+          } else {
+            unsigned long long v[kMaxSubC];
+            for (int q = 0; q < hdr->n_sub; ++q) v[q] = vload(&hdr->acc[q]);
+            write_unit_outputs(P, c, hdr->field, hdr->kind, hdr->j, hdr->n_uw, v);
+          }
+        }
+        atomicAdd(&SS->pending, ~0ull);
       }
       __syncthreads();
       continue;
     }
-    const int64_t N = U.N;
-    uint64_t* A0;
-    uint64_t* B0;
-    if (N <= sm_elems) { A0 = ebuf; B0 = ebuf + sm_elems; }
-    else { A0 = gbuf; B0 = gbuf + P.elem_cap; }
-    const int64_t kbase = U.key_lo;
 
-    // ---------------- emission: each thread owns a contiguous element range
-    // (one binary search for its first run, then a cursor), outer-tuple
-    // decode in 32-bit arithmetic when the run's extents allow it.
+    // ================= unsplit unit: one sort in shared (or slab) memory =================
     {
-      const int64_t per = (N + kNT - 1) / kNT;
-      const int64_t e0 = min(N, (int64_t)threadIdx.x * per), e1 = min(N, e0 + per);
-      int ri = 0;
-      if (e0 < e1) {
-        int lo = 0, hi = nr - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (roff[mid] <= e0) lo = mid; else hi = mid - 1;
+      const int64_t c = U.cfg;
+      const Geo& G = P.geos[c];
+      const gvo_config cfg = P.cfgs[c];
+      const int tpl = cfg.template_id;
+      const int abase = P.T.acc_base[tpl];
+      const int64_t* fbase = P.T.field_base + P.T.field_base_off[tpl];
+      const int32_t bd[3] = {cfg.block[0], cfg.block[1], cfg.block[2]};
+      const int64_t gd[3] = {cfg.grid[0], cfg.grid[1], cfg.grid[2]};
+      const Granule Gr = Granule::make(U.g);
+      const int64_t tpb = G.tpb;
+      const int nr = min(U.n_runs, (int)P.run_cap);
+      int64_t* roff = nr <= kSmemRuns ? roff_sh : roff_gl;
+      const long long t_runs = t_start;
+    const int64_t N = U.N;
+      uint64_t* A0;
+      uint64_t* B0;
+      if (N <= sm_elems) { A0 = ebuf; B0 = ebuf + sm_elems; }
+      else { A0 = gbuf; B0 = gbuf + P.elem_cap; }
+      const int64_t kbase = U.key_lo;
+
+      // ---------------- emission: each thread owns a contiguous element range
+      // (one binary search for its first run, then a cursor), outer-tuple
+      // decode in 32-bit arithmetic when the run's extents allow it.
+      {
+        const int64_t per = (N + kNT - 1) / kNT;
+        const int64_t e0 = min(N, (int64_t)threadIdx.x * per), e1 = min(N, e0 + per);
+        int ri = 0;
+        if (e0 < e1) {
+          int lo = 0, hi = nr - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (roff[mid] <= e0) lo = mid; else hi = mid - 1;
+          }
+          ri = lo;
         }
-        ri = lo;
-      }
-      for (int64_t i = e0; i < e1; ++i) {
-        while (roff[ri + 1] <= i) ++ri;
-        const Run& r = runs[ri];
-        int64_t k = i - roff[ri];
-        int64_t glo, ghi;
-        if (r.kind == 0) {
-          int64_t piece = 0;
-          if (r.pieces > 1) { piece = k % r.pieces; k /= r.pieces; }
-          uint64_t b = (uint64_t)r.base;
-          if (k < (int64_t(1) << 31)) {
-            uint32_t k32 = (uint32_t)k;
-            for (int d = r.nd - 1; d >= 0; --d) {
-              const uint32_t ex = (uint32_t)r.ext[d];
-              const uint32_t q = ex ? k32 / ex : 0;
-              b += (uint64_t)r.stride[d] * (uint64_t)(k32 - q * ex);
-              k32 = q;
+        for (int64_t i = e0; i < e1; ++i) {
+          while (roff[ri + 1] <= i) ++ri;
+          const Run& r = runs[ri];
+          int64_t k = i - roff[ri];
+          int64_t glo, ghi;
+          if (r.kind == 0) {
+            int64_t piece = 0;
+            if (r.pieces > 1) { piece = k % r.pieces; k /= r.pieces; }
+            uint64_t b = (uint64_t)r.base;
+            if (k < (int64_t(1) << 31)) {
+              uint32_t k32 = (uint32_t)k;
+              for (int d = r.nd - 1; d >= 0; --d) {
+                const uint32_t ex = (uint32_t)r.ext[d];
+                const uint32_t q = ex ? k32 / ex : 0;
+                b += (uint64_t)r.stride[d] * (uint64_t)(k32 - q * ex);
+                k32 = q;
+              }
+            } else {
+              for (int d = r.nd - 1; d >= 0; --d) {
+                const int64_t idx = k % r.ext[d];
+                k /= r.ext[d];
+                b += (uint64_t)r.stride[d] * (uint64_t)idx;
+              }
+            }
+            glo = Gr.of((int64_t)b);
+            ghi = Gr.of((int64_t)(b + r.span));
+            if (r.pieces > 1) {
+              int64_t plo = glo + piece * kPiece;
+              if (plo > ghi) plo = glo;
+              const int64_t phi = min(ghi, plo + kPiece - 1);
+              glo = plo;
+              ghi = phi;
             }
           } else {
-            for (int d = r.nd - 1; d >= 0; --d) {
-              const int64_t idx = k % r.ext[d];
-              k /= r.ext[d];
-              b += (uint64_t)r.stride[d] * (uint64_t)idx;
-            }
+            const int64_t blk = r.run_start + k / tpb;
+            const int64_t th = k % tpb;
+            int64_t crd[6];
+            crd[0] = th % bd[0];
+            crd[1] = (th / bd[0]) % bd[1];
+            crd[2] = th / ((int64_t)bd[0] * bd[1]);
+            crd[3] = blk % gd[0];
+            crd[4] = (blk / gd[0]) % gd[1];
+            crd[5] = blk / (gd[0] * gd[1]);
+            const int ga = abase + r.access;
+            glo = ghi = Gr.of(eval_point(P.T.code + P.T.code_off[ga], P.T.code_len[ga], crd, bd, fbase));
           }
-          glo = Gr.of((int64_t)b);
-          ghi = Gr.of((int64_t)(b + r.span));
-          if (r.pieces > 1) {
-            int64_t plo = glo + piece * kPiece;
-            if (plo > ghi) plo = glo;
-            const int64_t phi = min(ghi, plo + kPiece - 1);
-            glo = plo;
-            ghi = phi;
-          }
-        } else {
-          const int64_t blk = r.run_start + k / tpb;
-          const int64_t th = k % tpb;
-          int64_t crd[6];
-          crd[0] = th % bd[0];
-          crd[1] = (th / bd[0]) % bd[1];
-          crd[2] = th / ((int64_t)bd[0] * bd[1]);
-          crd[3] = blk % gd[0];
-          crd[4] = (blk / gd[0]) % gd[1];
-          crd[5] = blk / (gd[0] * gd[1]);
-          const int ga = abase + r.access;
-          glo = ghi = Gr.of(eval_point(P.T.code + P.T.code_off[ga], P.T.code_len[ga], crd, bd, fbase));
+          A0[i] = ((uint64_t)(glo - kbase) << kKeyShift) | ((uint64_t)(ghi - glo) << kTagBits) |
+                  (uint64_t)r.tag;
         }
-        A0[i] = ((uint64_t)(glo - kbase) << kKeyShift) | ((uint64_t)(ghi - glo) << kTagBits) |
-                (uint64_t)r.tag;
       }
-    }
-    __syncthreads();
+      __syncthreads();
 
-    const long long t_emit = clock64();
-    // ---------------- sort + sweeps
-    int kb = 0;
-    {
-      uint64_t span = (uint64_t)(U.key_hi - kbase);
-      while (span) { ++kb; span >>= 1; }
-    }
-    const int nbits = ((kb + 7) / 8) * 8;
-    const uint64_t* sorted = cta_sort(A0, B0, N, kKeyShift, nbits, hist, tot);
-    const long long t_sort = clock64();
-    sweep(sorted, N, U, wmax);
-    const long long t_sweep = clock64();
-
-    // ---------------- outputs
-    if (threadIdx.x == 0 && P.unit_stats) {
-      int64_t* us = P.unit_stats + item * 10;
-      us[6] = t_runs - t_start;
-      us[7] = t_emit - t_runs;
-      us[8] = t_sort - t_emit;
-      us[9] = t_sweep - t_sort;
-      us[0] = nr;
-      us[1] = N;
-      us[2] = N <= sm_elems;
-      us[3] = clock64() - t_start;
-      us[4] = nbits;
-      unsigned smid;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      us[5] = smid;
-    }
-    if (threadIdx.x == 0) {
-      const int f = U.field;
-      if (P.mode == 0) {
-        int64_t* row = P.counts + c * P.counts_stride;
-        if (U.kind == 0) {
-          int64_t* b = row + GVO_C_HDR + ((int64_t)U.j * P.F_stride + f) * 5;
-          b[0] = U.sub_val[0];
-          b[2] = U.sub_val[1];
-          b[3] = U.sub_val[2];
-        } else {
-          int64_t* wv = row + GVO_C_HDR + (int64_t)P.S_req * P.F_stride * 5;
-          for (int u = 0; u < G.n_uw; ++u) {
-            int64_t* o = wv + ((int64_t)u * P.F_stride + f) * 4;
-            o[0] = U.sub_val[4 * u + 0];
-            o[1] = U.sub_val[4 * u + 1];
-            o[2] = U.sub_val[4 * u + 2];
-            o[3] = u ? U.sub_val[4 * u] + U.sub_val[4 * (u - 1)] - U.sub_val[4 * u + 3] : 0;
-          }
-        }
-      } else if (P.mode == 1) {
-        for (int u = 0; u < G.n_uw; ++u) {
-          int64_t* o = P.counts + ((int64_t)u * P.F_stride + f) * 4;
-          o[0] = U.sub_val[4 * u + 0];
-          o[1] = U.sub_val[4 * u + 1];
-          o[2] = U.sub_val[4 * u + 2];
-          o[3] = u ? U.sub_val[4 * u] + U.sub_val[4 * (u - 1)] - U.sub_val[4 * u + 3] : 0;
-        }
-      } else {
-        P.counts[f * 2 + 0] = U.sub_val[0];
-        P.counts[f * 2 + 1] = U.sub_val[1];
+      const long long t_emit = clock64();
+      // ---------------- sort + sweeps
+      int kb = 0;
+      {
+        uint64_t span = (uint64_t)(U.key_hi - kbase);
+        while (span) { ++kb; span >>= 1; }
       }
+      const int nbits = ((kb + 7) / 8) * 8;
+      const uint64_t* sorted = cta_sort(A0, B0, N, kKeyShift, nbits, hist, tot);
+      const long long t_sort = clock64();
+      sweep(sorted, N, U, wmax);
+      const long long t_sweep = clock64();
+
+      // ---------------- outputs
+      if (threadIdx.x == 0 && P.unit_stats) {
+        int64_t* us = P.unit_stats + item * 10;
+        us[6] = t_runs - t_start;
+        us[7] = t_emit - t_runs;
+        us[8] = t_sort - t_emit;
+        us[9] = t_sweep - t_sort;
+        us[0] = nr;
+        us[1] = N;
+        us[2] = N <= sm_elems;
+        us[3] = clock64() - t_start;
+        us[4] = nbits;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        us[5] = smid;
+      }
+      if (threadIdx.x == 0) {
+        unsigned long long v[kMaxSubC];
+        for (int q = 0; q < U.n_sub; ++q) v[q] = (unsigned long long)U.sub_val[q];
+        write_unit_outputs(P, c, U.field, U.kind, U.j, P.mode == 2 ? 0 : G.n_uw, v);
+        if (SS) atomicAdd(&SS->pending, ~0ull);
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
@@ -906,8 +1322,13 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st) {
   P.work = L.work;
   P.warp = L.warp;
   P.n_warp_items = L.n_warp_items;
+  P.split = L.split;
+  P.sm_cap = L.sm_cap;
+  static int32_t epoch = 0;
+  P.epoch = ++epoch == 0 ? ++epoch : epoch;  // never 0 (the zeroed initial state)
   if (P.n_items + P.n_warp_items <= 0) return;
   cudaMemsetAsync(P.work, 0, sizeof(unsigned long long), st);
+  if (P.split) cudaMemsetAsync(P.split, 0, 4 * sizeof(unsigned long long), st);  // head, tail, pending, arena_top
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sets, cudaFuncAttributeMaxDynamicSharedMemorySize, kSetsSmemBytes);
@@ -921,12 +1342,12 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st) {
 // bytes of the shared element buffer (what a fused warp item may use)
 int64_t sets_ebuf_bytes() {
   size_t off = (sizeof(UnitSh) + 15) & ~size_t(15);
-  off += kNW * 256 * 4 + 256 * 4 + kMaxSub * kNW * 8 + (kSmemRuns + 1) * 8 + kNW * kClassPts * 8;
+  off += kNW * 256 * 4 + 256 * 4 + kMaxSub * kNW * 8 + (kSmemRuns + 1) * 8 + kNW * kClassPts * 8 + kSmemRuns * 8;
   return (int64_t)kSetsSmemBytes - (int64_t)off;
 }
 
 int64_t sets_slab_bytes(int64_t run_cap, int64_t elem_cap) {
-  return ((run_cap * (int64_t)sizeof(Run) + (run_cap + 1) * 8 + 2 * elem_cap * 8) + 255) & ~int64_t(255);
+  return ((run_cap * (int64_t)sizeof(Run) + 2 * (run_cap + 1) * 8 + 2 * elem_cap * 8) + 255) & ~int64_t(255);
 }
 
 }  // namespace gvo

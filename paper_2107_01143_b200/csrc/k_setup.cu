@@ -54,62 +54,66 @@ __device__ inline int representative(const int64_t g[3], int samples, int64_t* o
   return cnt;
 }
 
-// Coefficient classes of every (field, kind) slot (one warp).  Lanes find
-// each access's representative (first earlier access of the slot with the
-// same coefficients); lane 0 numbers the classes in slot order; lanes then
-// gather each class's constants and sort them (insertion sort, unique).
-__device__ void build_classes(const TplView& T, int tpl, const int64_t* crow, CTab ct, int16_t* rep_of) {
-  const int lane = threadIdx.x & 31;
+// Coefficient classes of every (field, kind) slot, all threads of the CTA.
+// Representatives (first earlier access of the slot with identical
+// coefficients) per access, member counts per representative, class
+// numbering in slot order (thread 0, O(A)), then each class's constants
+// gathered and sorted (insertion sort, unique) by one thread per class.
+__device__ void build_classes_cta(const TplView& T, int tpl, const int64_t* crow, CTab ct, int16_t* rep_of,
+                                  int16_t* members) {
   const int32_t* fko = T.fk_off + tpl * (2 * kMaxFields + 1);
-  for (int slot = 0; slot < 2 * kMaxFields; ++slot) {
-    const int b = fko[slot], e = fko[slot + 1];
-    for (int q = b + lane; q < e; q += 32) {
-      const int a = T.fk_list[q];
-      const int64_t* ca = crow + a * 8;
-      int64_t r = -1;
-      if (ca[7] == kAffine) {
-        r = a;
-        for (int q2 = b; q2 < q; ++q2) {
-          const int a2 = T.fk_list[q2];
-          const int64_t* cb = crow + a2 * 8;
-          if (cb[7] != kAffine) continue;
-          bool same = true;
-          for (int k = 1; k < 7; ++k) same &= cb[k] == ca[k];
-          if (same) { r = a2; break; }
-        }
+  const int A = T.n_acc[tpl];
+  const int abase = T.acc_base[tpl];
+  for (int a = threadIdx.x; a < A; a += blockDim.x) {
+    const int slot = T.acc_field[abase + a] * 2 + T.acc_kind[abase + a];
+    const int64_t* ca = crow + a * 8;
+    int r = -1;
+    if (ca[7] == kAffine) {
+      r = a;
+      for (int q2 = fko[slot]; q2 < fko[slot + 1]; ++q2) {
+        const int a2 = T.fk_list[q2];
+        if (a2 == a) break;
+        const int64_t* cb = crow + a2 * 8;
+        if (cb[7] != kAffine) continue;
+        bool same = true;
+        for (int k = 1; k < 7; ++k) same &= cb[k] == ca[k];
+        if (same) { r = a2; break; }
       }
-      rep_of[a] = (int16_t)r;
     }
+    rep_of[a] = (int16_t)r;
   }
-  __syncwarp();
-  if (lane == 0) {
+  __syncthreads();
+  for (int a = threadIdx.x; a < A; a += blockDim.x) {
+    int cnt = 0;
+    if (rep_of[a] == a)
+      for (int b = 0; b < A; ++b) cnt += rep_of[b] == a;
+    members[a] = (int16_t)cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
     int64_t ncls = 0, off = 0;
     for (int slot = 0; slot < 2 * kMaxFields; ++slot) {
       ct.slot_first()[slot] = ncls;
-      const int b = fko[slot], e = fko[slot + 1];
-      for (int q = b; q < e; ++q) {
+      for (int q = fko[slot]; q < fko[slot + 1]; ++q) {
         const int a = T.fk_list[q];
         if (rep_of[a] != a) continue;
-        int64_t members = 0;
-        for (int q2 = q; q2 < e; ++q2) members += rep_of[T.fk_list[q2]] == a;
         ct.rep()[ncls] = a;
         ct.start()[ncls] = off;
-        ct.cnt()[ncls] = members;
-        off += members;
+        ct.cnt()[ncls] = members[a];
+        off += members[a];
         ++ncls;
       }
     }
     ct.slot_first()[2 * kMaxFields] = ncls;
   }
-  __syncwarp();
+  __syncthreads();
   const int64_t ncls = ct.slot_first()[2 * kMaxFields];
-  for (int64_t c = lane; c < ncls; c += 32) {
+  for (int64_t c = threadIdx.x; c < ncls; c += blockDim.x) {
     const int64_t r = ct.rep()[c];
-    const int f = T.acc_field[T.acc_base[tpl] + r], k = T.acc_kind[T.acc_base[tpl] + r];
-    const int b = fko[f * 2 + k], e = fko[f * 2 + k + 1];
+    const int slot = T.acc_field[abase + r] * 2 + T.acc_kind[abase + r];
     int64_t* P = ct.pts() + ct.start()[c];
     int64_t n = 0;
-    for (int q = b; q < e; ++q) {
+    for (int q = fko[slot]; q < fko[slot + 1]; ++q) {
       const int a = T.fk_list[q];
       if (rep_of[a] != r) continue;
       const int64_t v = crow[a * 8];
@@ -126,12 +130,23 @@ __device__ void build_classes(const TplView& T, int tpl, const int64_t* crow, CT
     }
     ct.cnt()[c] = n;
   }
+  __syncthreads();
 }
 
-__global__ void k_setup(TplView T, const gvo_machine* machines, const gvo_config* cfgs,
-                        int64_t n, gvo_sampling smp, int64_t* coefs, Geo* geos, int64_t* ctabs) {
-  const int lane = threadIdx.x & 31;
-  const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+// evaluation-order key of a (phase, group, access) overflow failure
+__device__ __forceinline__ unsigned long long fail_key(int phase, int gorder, int f, int kind, int a) {
+  return ((unsigned long long)phase << 56) | ((unsigned long long)gorder << 40) |
+         ((unsigned long long)(f * 2 + kind) << 16) | (unsigned long long)a;
+}
+
+// One CTA per configuration.
+__global__ void __launch_bounds__(256) k_setup(TplView T, const gvo_machine* machines, const gvo_config* cfgs,
+                                               int64_t n, gvo_sampling smp, int64_t* coefs, Geo* geos,
+                                               int64_t* ctabs) {
+  extern __shared__ int16_t sh16[];
+  __shared__ Geo G;
+  __shared__ unsigned long long first_fail;
+  const int64_t c = blockIdx.x;
   if (c >= n) return;
   const gvo_config cfg = cfgs[c];
   const int tpl = cfg.template_id;
@@ -144,94 +159,174 @@ __global__ void k_setup(TplView T, const gvo_machine* machines, const gvo_config
   const int64_t gd[3] = {cfg.grid[0], cfg.grid[1], cfg.grid[2]};
   int64_t* crow = coefs + c * (int64_t)T.max_acc * 8;
 
-  // ---- coefficient tables (lane-parallel over accesses)
-  for (int a = lane; a < A; a += 32) {
+  // ---- coefficient tables (thread per access)
+  for (int a = threadIdx.x; a < A; a += blockDim.x) {
     const int ga = abase + a;
     AffineForm f;
     int flag = affine_extract(T.code + T.code_off[ga], T.code_len[ga], bd, fbase, &f);
     for (int k = 0; k < 7; ++k) crow[a * 8 + k] = flag == kAffine ? f.c[k] : 0;
     crow[a * 8 + 7] = flag;
   }
-  __syncwarp();
-  {
-    extern __shared__ int16_t sh_rep[];
-    build_classes(T, tpl, crow, CTab{ctabs + c * ctab_stride(T.max_acc), T.max_acc},
-                  sh_rep + (threadIdx.x >> 5) * T.max_acc);
+  __syncthreads();
+  build_classes_cta(T, tpl, crow, CTab{ctabs + c * ctab_stride(T.max_acc), T.max_acc}, sh16, sh16 + T.max_acc);
+
+  // ---- geometry (thread 0)
+  if (threadIdx.x == 0) {
+    G.phases = smp.phases ? smp.phases : 7;
+    G.status = GVO_OK;
+    G.err_phase = G.err_group = G.err_access = -1;
+    G.tpb = (int64_t)bd[0] * bd[1] * bd[2];
+    G.lups_per_block = G.tpb * cfg.work_per_thread;
+    G.total_blocks = gd[0] * gd[1] * gd[2];
+    G.n_samples = 0;
+    G.n_uw = 0;
+    G.n_pairs = 0;
+    G.has_pred = 0;
+    G.per_wave = 0;
+    G.n_waves = 0;
+    G.first_wave = 0;
+    G.l1_block = -1;
+    for (int f = 0; f < kMaxFields; ++f)
+      for (int j = 0; j < kMaxSamples; ++j) G.dup_of[f][j] = -1;
+    first_fail = ~0ull;
+    auto fail = [&](int status, int phase, int group, int access) {
+      G.status = status;
+      G.err_phase = phase;
+      G.err_group = group;
+      G.err_access = access;
+    };
+    // phase 0 geometry (volumes.py:152-185)
+    if (G.phases & 1) {
+      if (smp.block_samples < 1) fail(GVO_ERR_FOOTPRINT, 0, -1, 0);
+      else {
+        const int ns = representative(gd, smp.block_samples, G.sample_lin, kMaxSamples);
+        if (ns < 0) fail(GVO_ERR_UNSUPPORTED, 0, -1, 0);
+        else G.n_samples = ns;
+      }
+    }
+    // phase 1 geometry (footprint.py:48-78, 616-637); its FootprintErrors are
+    // raised only if phase 0 passes the overflow guard (resolved below)
+    if (G.status == GVO_OK && (G.phases & 2)) {
+      int64_t per_wave = smp.blocks_per_wave_override;
+      int err = -1;
+      if (smp.wave_samples < 1) err = 0;
+      else if (per_wave == 0) {
+        if (G.tpb > m.max_threads_per_block) err = 1;
+        else {
+          int64_t per_sm = m.max_threads_per_sm / G.tpb;
+          if (m.max_blocks_per_sm < per_sm) per_sm = m.max_blocks_per_sm;
+          if (per_sm < 1) err = 2;
+          else per_wave = m.sm_count * per_sm;
+        }
+      }
+      if (err < 0 && per_wave < 1) err = 3;
+      if (err >= 0) {
+        G.err_access = err;  // pending: becomes the status unless phase 0 fails first
+        G.err_phase = 1;
+        G.n_uw = 0;
+      } else {
+        G.per_wave = per_wave;
+        G.n_waves = (G.total_blocks + per_wave - 1) / per_wave;
+        if (G.n_waves == 1) {
+          G.n_pairs = 1;
+          G.has_pred = 0;
+          G.n_uw = 1;
+          G.first_wave = 0;
+        } else {
+          const int64_t hi = G.n_waves >= 3 ? G.n_waves - 2 : G.n_waves - 1;
+          const int64_t count = smp.wave_samples < hi ? smp.wave_samples : hi;
+          const int64_t mid = (1 + hi) / 2;
+          int64_t start = mid - (count - 1) / 2;
+          if (start < 1) start = 1;
+          if (start > hi - count + 1) start = hi - count + 1;
+          if (count + 1 > kMaxUWaves) { G.err_access = 100; G.err_phase = 1; }
+          else {
+            G.n_pairs = (int)count;
+            G.has_pred = 1;
+            G.n_uw = (int)count + 1;
+            G.first_wave = start - 1;
+          }
+        }
+        for (int u = 0; u < G.n_uw; ++u) {
+          const int64_t w = G.first_wave + u;
+          G.uw_start[u] = w * per_wave;
+          const int64_t rem = G.total_blocks - G.uw_start[u];
+          G.uw_count[u] = rem < per_wave ? rem : per_wave;
+        }
+      }
+    }
+    // phase 2 geometry: representative_blocks(k, 5)[len // 2]
+    if (G.status == GVO_OK && (G.phases & 4)) {
+      int64_t picks[5];
+      const int np = representative(gd, 5, picks, 5);
+      G.l1_block = picks[np / 2];
+    }
   }
+  __syncthreads();
 
-  // ---- geometry (computed redundantly by every lane; cheap and uniform)
-  Geo G;
-  G.phases = smp.phases ? smp.phases : 7;
-  G.status = GVO_OK;
-  G.err_phase = G.err_group = G.err_access = -1;
-  G.tpb = (int64_t)bd[0] * bd[1] * bd[2];
-  G.lups_per_block = G.tpb * cfg.work_per_thread;
-  G.total_blocks = gd[0] * gd[1] * gd[2];
-  G.n_samples = 0;
-  G.n_uw = 0;
-  G.n_pairs = 0;
-  G.has_pred = 0;
-  G.per_wave = 0;
-  G.n_waves = 0;
-  G.first_wave = 0;
-  G.l1_block = -1;
-
-  auto fail = [&](int status, int phase, int group, int access) {
-    G.status = status;
-    G.err_phase = phase;
-    G.err_group = group;
-    G.err_access = access;
-  };
-
-  // coordinate-bounds guard for one group over all accesses in the given
-  // order (by field then kernel order, optionally loads before stores);
-  // returns the first failing access position or -1.
-  auto guard = [&](int64_t rs, int64_t rc, int order) -> int {
-    int64_t clo[6], chi[6];
-    clo[0] = clo[1] = clo[2] = 0;
-    chi[0] = bd[0] - 1; chi[1] = bd[1] - 1; chi[2] = bd[2] - 1;
-    run_bid_bounds(rs, rc, gd, clo + 3, chi + 3);
-    int best = INT32_MAX;  // order key
-    int best_a = -1;
-    for (int a = lane; a < A; a += 32) {
+  // ---- overflow guard: thread per (group, access), first failure in the
+  // reference's evaluation order.  Groups: samples (order s), sampled waves
+  // (current of pair 0, its predecessor, then the other currents), L1 block.
+  if (G.status == GVO_OK) {
+    const int ns = (G.phases & 1) ? G.n_samples : 0;
+    const int nu = (G.phases & 2) ? G.n_uw : 0;
+    const int nl = (G.phases & 4) ? 1 : 0;
+    const int ng = ns + nu + nl;
+    for (int t = threadIdx.x; t < ng * A; t += blockDim.x) {
+      const int gi = t / A, a = t % A;
+      int phase, gorder, rs_idx;
+      int64_t rs, rc;
+      if (gi < ns) { phase = 0; gorder = gi; rs = G.sample_lin[gi]; rc = 1; rs_idx = gi; }
+      else if (gi < ns + nu) {
+        const int k = gi - ns;
+        const int u = G.n_uw == 1 ? 0 : (k == 0 ? 1 : (k == 1 ? 0 : k));
+        phase = 1; gorder = k; rs = G.uw_start[u]; rc = G.uw_count[u]; rs_idx = u;
+      } else { phase = 2; gorder = 0; rs = G.l1_block; rc = 1; rs_idx = 0; }
+      int64_t clo[6], chi[6];
+      clo[0] = clo[1] = clo[2] = 0;
+      chi[0] = bd[0] - 1; chi[1] = bd[1] - 1; chi[2] = bd[2] - 1;
+      run_bid_bounds(rs, rc, gd, clo + 3, chi + 3);
       const int ga = abase + a;
       int64_t lo, hi;
       if (bounds_check(T.code + T.code_off[ga], T.code_len[ga], clo, chi, bd, fbase, &lo, &hi) >= 0) {
-        // order 0: field-major, kernel order inside (volumes.py:164-171)
-        // order 1: field, loads before stores (footprint.py:541-545)
-        // order 2: kernel order (volumes.py:126)
-        const int f = order == 2 ? 0 : T.acc_field[ga];
-        const int kind = order == 1 ? T.acc_kind[ga] : 0;
-        const int key = (f * 2 + kind) * GVO_MAX_ACCESSES + a;
-        if (key < best) { best = key; best_a = a; }
+        // order inside a group: phase 0 field-major (volumes.py:164-171);
+        // phase 1 field, loads before stores (footprint.py:541-545);
+        // phase 2 kernel order (volumes.py:126)
+        const int f = phase == 2 ? 0 : T.acc_field[ga];
+        const int kind = phase == 1 ? T.acc_kind[ga] : 0;
+        unsigned long long key = fail_key(phase, gorder, f, kind, a);
+        key |= (unsigned long long)rs_idx << 32;  // carries the group index (determined by gorder)
+        atomicMin(&first_fail, key);
       }
     }
-    for (int o = 16; o; o >>= 1) {
-      int ob = __shfl_xor_sync(0xffffffffu, best, o);
-      int oa = __shfl_xor_sync(0xffffffffu, best_a, o);
-      if (ob < best) { best = ob; best_a = oa; }
-    }
-    return best_a;
-  };
-
-  // ---- phase 0: block samples (volumes.py:152-185)
-  if (!(G.phases & 1)) {
-    // not requested
-  } else if (smp.block_samples < 1) {
-    fail(GVO_ERR_FOOTPRINT, 0, -1, 0);  // "sample count must be >= 1"
-  } else {
-    int ns = representative(gd, smp.block_samples, G.sample_lin, kMaxSamples);
-    if (ns < 0) fail(GVO_ERR_UNSUPPORTED, 0, -1, 0);
-    else G.n_samples = ns;
   }
-  // ---- translation dedup of block samples (exact): all accesses of field f
-  // affine with one common block-coordinate coefficient vector, and the
-  // address shift between samples j and j' a multiple of the line size.
-  for (int f = 0; f < kMaxFields; ++f)
-    for (int j = 0; j < kMaxSamples; ++j) G.dup_of[f][j] = -1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long k = first_fail;
+    const int fphase = k == ~0ull ? 3 : (int)(k >> 56);
+    // resolve in evaluation order: phase-0 overflow, phase-1 footprint
+    // precondition, phase-1 overflow, phase-2 overflow
+    if (G.status == GVO_OK) {
+      const bool pending1 = G.err_phase == 1;
+      if (fphase == 0) {
+        G.status = GVO_ERR_ADDRESS_OVERFLOW; G.err_phase = 0;
+        G.err_group = (int)((k >> 32) & 0xff); G.err_access = (int)(k & 0xffff);
+      } else if (pending1) {
+        G.status = G.err_access == 100 ? GVO_ERR_UNSUPPORTED : GVO_ERR_FOOTPRINT;
+        if (G.err_access == 100) G.err_access = 0;
+        G.err_group = -1;
+      } else if (fphase <= 2) {
+        G.status = GVO_ERR_ADDRESS_OVERFLOW; G.err_phase = fphase;
+        G.err_group = (int)((k >> 32) & 0xff); G.err_access = (int)(k & 0xffff);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- translation dedup of block samples (thread per field)
   if (G.status == GVO_OK && (G.phases & 1)) {
     const int32_t* fko = T.fk_off + tpl * (2 * kMaxFields + 1);
-    for (int f = 0; f < F; ++f) {
+    for (int f = threadIdx.x; f < F; f += blockDim.x) {
       bool ok = true;
       const int64_t* c0 = nullptr;
       for (int q = fko[2 * f]; q < fko[2 * f + 2] && ok; ++q) {
@@ -250,111 +345,42 @@ __global__ void k_setup(TplView T, const gvo_machine* machines, const gvo_config
           const int64_t bi = G.sample_lin[i];
           const int64_t xi = bi % gd[0], yi = (bi / gd[0]) % gd[1], zi = bi / (gd[0] * gd[1]);
           const __int128 d = (__int128)c0[4] * (xj - xi) + (__int128)c0[5] * (yj - yi) + (__int128)c0[6] * (zj - zi);
-          const __int128 r = d % line;
-          if (r == 0) { G.dup_of[f][j] = (int8_t)i; break; }
+          if (d % line == 0) { G.dup_of[f][j] = (int8_t)i; break; }
         }
       }
     }
   }
-  if (G.status == GVO_OK && (G.phases & 1)) {
-    for (int s = 0; s < G.n_samples; ++s) {
-      int a = guard(G.sample_lin[s], 1, 0);
-      if (a >= 0) { fail(GVO_ERR_ADDRESS_OVERFLOW, 0, s, a); break; }
-    }
+  __syncthreads();
+  // copy the plan out
+  {
+    const int words = (int)(sizeof(Geo) / 4);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(&G);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(geos + c);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
   }
-
-  // ---- phase 1: waves (volumes.py:203-250)
-  if (G.status == GVO_OK && (G.phases & 2)) {
-    int64_t per_wave = smp.blocks_per_wave_override;
-    if (smp.wave_samples < 1) {
-      fail(GVO_ERR_FOOTPRINT, 1, -1, 0);
-    } else if (per_wave == 0) {
-      // blocks_per_wave (footprint.py:48-57)
-      if (G.tpb > m.max_threads_per_block) fail(GVO_ERR_FOOTPRINT, 1, -1, 1);
-      else {
-        int64_t per_sm = m.max_threads_per_sm / G.tpb;
-        if (m.max_blocks_per_sm < per_sm) per_sm = m.max_blocks_per_sm;
-        if (per_sm < 1) fail(GVO_ERR_FOOTPRINT, 1, -1, 2);
-        else per_wave = m.sm_count * per_sm;
-      }
-    }
-    if (G.status == GVO_OK && per_wave < 1) fail(GVO_ERR_FOOTPRINT, 1, -1, 3);
-    if (G.status == GVO_OK) {
-      G.per_wave = per_wave;
-      G.n_waves = (G.total_blocks + per_wave - 1) / per_wave;
-      int64_t start, count;
-      if (G.n_waves == 1) {
-        G.n_pairs = 1;
-        G.has_pred = 0;
-        G.n_uw = 1;
-        G.first_wave = 0;
-      } else {
-        const int64_t hi = G.n_waves >= 3 ? G.n_waves - 2 : G.n_waves - 1;
-        const int64_t lo = 1;
-        count = smp.wave_samples < hi - lo + 1 ? smp.wave_samples : hi - lo + 1;
-        const int64_t mid = (lo + hi) / 2;
-        start = mid - (count - 1) / 2;
-        if (start < lo) start = lo;
-        if (start > hi - count + 1) start = hi - count + 1;
-        if (count + 1 > kMaxUWaves) fail(GVO_ERR_UNSUPPORTED, 1, -1, 0);
-        G.n_pairs = (int)count;
-        G.has_pred = 1;
-        G.n_uw = (int)count + 1;
-        G.first_wave = start - 1;
-      }
-      if (G.status == GVO_OK) {
-        for (int u = 0; u < G.n_uw; ++u) {
-          const int64_t w = G.first_wave + u;
-          G.uw_start[u] = w * per_wave;
-          const int64_t rem = G.total_blocks - G.uw_start[u];
-          G.uw_count[u] = rem < per_wave ? rem : per_wave;
-        }
-        // evaluation order: current of pair 0, its predecessor, then the
-        // remaining currents (cached summaries are not re-evaluated)
-        for (int k = 0; k < G.n_uw && G.status == GVO_OK; ++k) {
-          int u = G.n_uw == 1 ? 0 : (k == 0 ? 1 : (k == 1 ? 0 : k));
-          int a = guard(G.uw_start[u], G.uw_count[u], 1);
-          if (a >= 0) fail(GVO_ERR_ADDRESS_OVERFLOW, 1, u, a);
-        }
-      }
-    }
-  }
-
-  // ---- phase 2: L1 block = representative_blocks(k, 5)[len // 2]
-  if (G.status == GVO_OK && (G.phases & 4)) {
-    int64_t picks[5];
-    int np = representative(gd, 5, picks, 5);
-    G.l1_block = picks[np / 2];
-    int a = guard(G.l1_block, 1, 2);
-    if (a >= 0) fail(GVO_ERR_ADDRESS_OVERFLOW, 2, 0, a);
-  }
-  if (lane == 0) geos[c] = G;
 }
 
 void launch_setup(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs,
                   int64_t n, const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos, int64_t* d_ctabs,
                   cudaStream_t st) {
-  const int wpb = 4;
-  const int64_t blocks = (n + wpb - 1) / wpb;
-  if (blocks > 0)
-    k_setup<<<(unsigned)blocks, wpb * 32, wpb * T.max_acc * sizeof(int16_t), st>>>(T, d_machines, d_cfgs, n, smp,
-                                                                                   d_coefs, d_geos, d_ctabs);
+  if (n > 0)
+    k_setup<<<(unsigned)n, 256, 2 * T.max_acc * sizeof(int16_t), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs,
+                                                                       d_geos, d_ctabs);
 }
 
 __global__ void k_classes_only(TplView T, const gvo_config* cfgs, int64_t n, const int64_t* coefs,
                                int64_t* ctabs) {
-  const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t c = blockIdx.x;
   if (c >= n) return;
   extern __shared__ int16_t sh_rep2[];
-  build_classes(T, cfgs[c].template_id, coefs + c * (int64_t)T.max_acc * 8,
-                CTab{ctabs + c * ctab_stride(T.max_acc), T.max_acc}, sh_rep2 + (threadIdx.x >> 5) * T.max_acc);
+  build_classes_cta(T, cfgs[c].template_id, coefs + c * (int64_t)T.max_acc * 8,
+                    CTab{ctabs + c * ctab_stride(T.max_acc), T.max_acc}, sh_rep2, sh_rep2 + T.max_acc);
 }
 
 void launch_classes(const TplView& T, const gvo_config* d_cfgs, int64_t n, const int64_t* d_coefs,
                     int64_t* d_ctabs, cudaStream_t st) {
   if (n > 0)
-    k_classes_only<<<(unsigned)((n + 3) / 4), 128, 4 * T.max_acc * sizeof(int16_t), st>>>(T, d_cfgs, n, d_coefs,
-                                                                                          d_ctabs);
+    k_classes_only<<<(unsigned)n, 128, 2 * T.max_acc * sizeof(int16_t), st>>>(T, d_cfgs, n, d_coefs, d_ctabs);
 }
 
 }  // namespace gvo

@@ -189,3 +189,33 @@ def test_lbm_and_layout_variants_vs_oracle():
         ev = ora.evaluate_kernel(k, m)
         assert p.glups == ev["glups"] and p.limiter == ev["limiter"]
         assert p.volumes.dram_load.v_down == ev["volumes"]["dram_load"]["down"]
+
+
+def test_errors_match_reference_class_and_message():
+    for case in load("errors"):
+        k = gvo.kernel_from_dict(case["spec"])
+        m = machine_from_dict(case["machine"])
+        try:
+            gvo.evaluate_kernel(k, m, **case["kw"])
+            got = None
+        except Exception as exc:  # noqa: BLE001
+            got = [type(exc).__name__, str(exc)]
+        assert got == case["error"], (case["spec"]["accesses"], case["kw"], got)
+
+
+def test_split_ranges_forced_small_capacity():
+    """Run the parity checks in a subprocess whose engine may keep only 96
+    intervals in shared memory: every unit then splits into many key ranges
+    (queued to other CTAs, clipped, re-split) — results must not change."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, GVO_SMEM_ELEMS="96")
+    tests = ["tests/test_gpu_parity.py::test_footprints_match_reference_golden",
+             "tests/test_gpu_parity.py::test_block_and_wave_integers_vs_reference",
+             "tests/test_gpu_parity.py::test_rank_sweep_order_identical_to_reference",
+             "tests/test_gpu_parity.py::test_random_kernels_vs_oracle"]
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", *tests], env=env,
+                       capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

@@ -218,9 +218,54 @@ def sweeps():
     return out
 
 
+def errors():
+    """Failing evaluations: exception class and message of the reference."""
+    from gvo import parse
+
+    out = []
+    v100 = gvo.v100_preset()
+
+    def case(fields, accs, block, grid, machine=v100, **kw):
+        names = [f.name for f in fields]
+        k = gvo.KernelDescriptor(fields=fields, accesses=tuple(gvo.Access(fn, kd, parse(t, fields=names))
+                                                                for fn, kd, t in accs),
+                                 launch=gvo.LaunchConfig(block, grid))
+        try:
+            gvo.evaluate_kernel(k, machine, **kw)
+            res = None
+        except Exception as exc:  # noqa: BLE001
+            res = [type(exc).__name__, str(exc)]
+        out.append({"spec": kernel_to_dict(k), "machine": machine_to_dict(machine), "kw": kw, "error": res})
+
+    fa = (gvo.Field("a", 8, (1 << 20,)),)
+    # phase 0: interior block bidx=2 overflows
+    case(fa, [("a", "load", "a + tidx * 8 + bidx * 4611686018427387904")], (4, 1, 1), (4, 1, 1))
+    # phase 1 only: interior blocks fine, the wave reaches bidx = 2
+    case(fa, [("a", "load", "a + tidx * 8 + bidx * 4611686018427387904")], (4, 1, 1), (3, 1, 1))
+    # a store overflowing after loads are fine (loads-before-stores order)
+    case(fa, [("a", "load", "a + tidx * 8"), ("a", "store", "a + bidy * 4611686018427387904 + tidx")], (4, 1, 1), (3, 3, 1))
+    # intermediate-node overflow that cancels at the root
+    case(fa, [("a", "load", "a + (tidx * 4611686018427387904 + bidx * 4611686018427387904) - bidx * 4611686018427387904")],
+         (4, 1, 1), (4, 1, 1))
+    # block larger than the machine limit -> FootprintError in the wave phase
+    case(fa, [("a", "load", "a + tidx * 8")], (1024, 2, 1), (1, 1, 1))
+    # samples < 1
+    case(fa, [("a", "load", "a + tidx * 8")], (32, 1, 1), (4, 4, 4), block_samples=0)
+    case(fa, [("a", "load", "a + tidx * 8")], (32, 1, 1), (4, 4, 4), wave_samples=0)
+    # override of 0 means computed; negative override is an error
+    case(fa, [("a", "load", "a + tidx * 8")], (32, 1, 1), (4, 4, 4), override_blocks_per_wave=-3)
+    # per-SM capacity
+    import dataclasses
+    small = dataclasses.replace(v100, max_threads_per_sm=512, max_threads_per_block=1024)
+    case(fa, [("a", "load", "a + tidx * 8")], (1024, 1, 1), (4, 1, 1), machine=small)
+    return out
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
-    what = sys.argv[1:] or ["footprints", "evaluations", "sweeps"]
+    what = sys.argv[1:] or ["footprints", "evaluations", "sweeps", "errors"]
+    if "errors" in what:
+        (OUT / "errors.json").write_text(json.dumps(errors()))
     if "footprints" in what:
         (OUT / "footprints.json").write_text(json.dumps(footprints()))
     if "evaluations" in what:

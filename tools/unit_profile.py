@@ -16,8 +16,11 @@ for _ in range(2):
     out = ctx.eval_configs_host(cfgs, 5, 2, 0)
 n_items = _native.C.c_int64()
 L.gvo_debug_units(ctx.h, 1, None, 0, _native.C.byref(n_items))
-st = np.zeros((n_items.value, 10), dtype=np.int64)
-L.gvo_debug_units(ctx.h, 0, _native._ptr(st), n_items.value, None)
+raw = np.zeros(n_items.value * 10 + 10 + 4096 * 10, dtype=np.int64)
+L.gvo_debug_units(ctx.h, 0, _native._ptr(raw), raw.size, None)
+st = raw[: n_items.value * 10].reshape(-1, 10)
+nrng = int(raw[n_items.value * 10])
+rng_rows = raw[n_items.value * 10 + 10: n_items.value * 10 + 10 + nrng * 10].reshape(-1, 10)
 F = out["F"]; S = out["S"]
 per_cfg = F * (S + 1)
 rows = []
@@ -41,3 +44,8 @@ for name, grp in (("wave", wave), ("block", blk)):
     ph = np.array([r[8] for r in grp], dtype=float)
     print(name, "phase Mcycles runs/emit/sort/sweep", (ph.sum(0) / 1e6).round(2), "mean", ph.mean(0).round(0))
 json.dump(rows, open(ROOT / "gpurun_out" / "unit_profile.json", "w"))
+print("ranges processed", nrng)
+if nrng:
+    rr = sorted(rng_rows.tolist(), key=lambda r: -r[4])
+    print("range cycles total M", sum(r[4] for r in rr) / 1e6, "max", rr[0][4])
+    for r in rr[:15]: print("desc", r[0], "a", r[1], "b", r[2], "N", r[3], "cyc", r[4], "nr", r[5], "sm", r[6], "cfg", kept[r[7]].key, "queued" if r[8] == 1 else "first")
