@@ -135,16 +135,19 @@ __device__ inline void emit_lattice(const RunSink& S, Lat L, int tag, const Gran
   const int64_t pieces = (len + kPiece - 1) / kPiece;
   const int slot = atomicAdd(S.n_runs, 1);
   if (slot >= S.cap) { atomicExch(S.status, GVO_ERR_CAPACITY); return; }
-  Run r;
-  r.base = L.base;
-  r.span = L.span;
-  r.nd = L.nd;
-  for (int d = 0; d < kMaxDims; ++d) { r.stride[d] = d < L.nd ? (int64_t)L.st[d] : 0; r.ext[d] = d < L.nd ? L.ex[d] : 1; }
-  r.tag = tag;
-  r.kind = 0;
-  r.access = -1;
-  r.pieces = pieces;
-  r.count = count * pieces;
+  Run* r = S.runs + slot;  // written field by field (no local struct copy)
+  r->base = L.base;
+  r->span = L.span;
+  r->nd = L.nd;
+  for (int d = 0; d < kMaxDims; ++d) {
+    r->stride[d] = d < L.nd ? (int64_t)L.st[d] : 0;
+    r->ext[d] = d < L.nd ? L.ex[d] : 1;
+  }
+  r->tag = tag;
+  r->kind = 0;
+  r->access = -1;
+  r->pieces = pieces;
+  r->count = count * pieces;
   // monotone: with dim 0 fastest, every dim's stride exceeds the span plus
   // the reach of all faster dims -> bases and interval ends increase with k
   {
@@ -154,71 +157,12 @@ __device__ inline void emit_lattice(const RunSink& S, Lat L, int tag, const Gran
       if (d > 0 && (unsigned __int128)L.st[d] <= reach) mono = false;
       reach += (unsigned __int128)L.st[d] * (uint64_t)(L.ex[d] - 1);
     }
-    r.mono = mono ? 1 : 0;
+    r->mono = mono ? 1 : 0;
   }
-  r.run_start = r.run_count = 0;
-  S.runs[slot] = r;
+  r->run_start = r->run_count = 0;
   atomicMin((long long*)S.key_lo, (long long)G.of(L.base));
   atomicMax((long long*)S.key_hi, (long long)G.of((int64_t)((uint64_t)L.base + ext_span)));
 }
-
-// Cover the translates P[0..n) (sorted, unique) of one lattice.  Rays along
-// an outer dimension extend that dimension; remaining points cluster when
-// consecutive gaps are <= span + g (their union keeps all gaps <= g).
-__device__ inline void cover_and_emit(const RunSink& S, const Lat& L0, const int64_t* P, int n,
-                                      int tag, const Granule& G) {
-  uint64_t req = n >= 64 ? ~0ull : ((1ull << n) - 1);
-  for (int d = L0.nd - 1; d >= 0 && req; --d) {
-    const int64_t s = (int64_t)L0.st[d];
-    for (int i = 0; i < n; ++i) {
-      if (contains(P, n, P[i] - s)) continue;  // not a ray start
-      uint64_t mem = 1ull << i;
-      int len = 1;
-      int64_t v = P[i];
-      while (true) {
-        // position of v + s
-        int lo = 0, hi = n - 1, pos = -1;
-        const int64_t t = v + s;
-        while (lo <= hi) {
-          int mid = (lo + hi) >> 1;
-          if (P[mid] == t) { pos = mid; break; }
-          if (P[mid] < t) lo = mid + 1; else hi = mid - 1;
-        }
-        if (pos < 0) break;
-        mem |= 1ull << pos;
-        ++len;
-        v = t;
-      }
-      if (len >= 2 && __popcll(mem & req) >= 2) {
-        Lat L = L0;
-        L.base = P[i];
-        L.ex[d] += len - 1;
-        emit_lattice(S, L, tag, G);
-        req &= ~mem;
-      }
-    }
-  }
-  if (!req) return;
-  // clusters over all points (covered ones act as bridges)
-  int i = 0;
-  while (i < n) {
-    int j = i;
-    uint64_t mem = 1ull << i;
-    while (j + 1 < n && (unsigned __int128)(uint64_t)(P[j + 1] - P[j]) <=
-                            (unsigned __int128)L0.span + (uint64_t)G.g) {
-      ++j;
-      mem |= 1ull << j;
-    }
-    if (mem & req) {
-      Lat L = L0;
-      L.base = P[i];
-      L.span = L0.span + (uint64_t)(P[j] - P[i]);
-      emit_lattice(S, L, tag, G);
-    }
-    i = j + 1;
-  }
-}
-
 
 // Warp-cooperative version: the class's translates P[0..n) (n <= 64, sorted,
 // unique) live in shared memory.  Rays of one dimension are disjoint (every
@@ -261,6 +205,54 @@ __device__ void cover_warp(const RunSink& S, const Lat& L0, const int64_t* P, in
     const unsigned lo32 = __reduce_or_sync(0xffffffffu, (unsigned)clear);
     const unsigned hi32 = __reduce_or_sync(0xffffffffu, (unsigned)(clear >> 32));
     req &= ~(((uint64_t)hi32 << 32) | lo32);
+  }
+  // rays along a stride that is not a lattice dimension (e.g. +-z offsets of
+  // a one-layer block): the smallest gap between consecutive uncovered
+  // translates, if wider than span + g, becomes an added dimension
+  const unsigned __int128 tol0 = (unsigned __int128)L0.span + (uint64_t)G.g;
+  for (int iter = 0; iter < 3 && __popcll(req) >= 2 && L0.nd < kMaxDims; ++iter) {
+    int64_t gap = INT64_MAX;
+    for (int i = lane; i < n; i += 32) {
+      if (!((req >> i) & 1ull)) continue;
+      int k = i + 1;
+      while (k < n && !((req >> k) & 1ull)) ++k;
+      if (k < n) gap = min(gap, P[k] - P[i]);
+    }
+    for (int o = 16; o; o >>= 1) gap = min(gap, __shfl_xor_sync(0xffffffffu, gap, o));
+    if (gap == INT64_MAX || (unsigned __int128)(uint64_t)gap <= tol0) break;
+    uint64_t clear = 0;
+    for (int i = lane; i < n; i += 32) {
+      if (contains(P, n, P[i] - gap)) continue;
+      uint64_t mem = 1ull << i;
+      int len = 1, pos = i;
+      while (pos + 1 < n) {
+        const int64_t t = P[pos] + gap;
+        int lo = pos + 1, hi = n - 1, f = -1;
+        while (lo <= hi) {
+          const int mid = (lo + hi) >> 1;
+          if (P[mid] == t) { f = mid; break; }
+          if (P[mid] < t) lo = mid + 1; else hi = mid - 1;
+        }
+        if (f < 0) break;
+        mem |= 1ull << f;
+        ++len;
+        pos = f;
+      }
+      if (len >= 2 && __popcll(mem & req) >= 2) {
+        Lat L = L0;
+        L.base = P[i];
+        L.st[L.nd] = (uint64_t)gap;
+        L.ex[L.nd] = len;
+        ++L.nd;
+        emit_lattice(S, L, tag, G);
+        clear |= mem;
+      }
+    }
+    const unsigned lo32 = __reduce_or_sync(0xffffffffu, (unsigned)clear);
+    const unsigned hi32 = __reduce_or_sync(0xffffffffu, (unsigned)(clear >> 32));
+    const uint64_t cl = ((uint64_t)hi32 << 32) | lo32;
+    if (!cl) break;
+    req &= ~cl;
   }
   if (!req) return;
   const unsigned __int128 tol = (unsigned __int128)L0.span + (uint64_t)G.g;
@@ -576,9 +568,203 @@ struct SetsArgs {
   int32_t epoch;            // launch number; queue slots are ready when ready == epoch
 };
 
+// ------------------------------------------------------------------ micro tier
+// Small units (one field of one sample block, typically 50-500 intervals)
+// are processed by ONE warp: 16 units per CTA concurrently.  The warp builds
+// the unit's lattices (warp-cooperative cover), emits the intervals into its
+// own shared-memory slice, bitonic-sorts them in place (the sweep needs key
+// order only, not stability) and sweeps.  Units that do not fit fall back to
+// the CTA path.
+constexpr int kMicroElems = 512;
+constexpr int kMicroRuns = 64;          // run offsets kept per warp
+constexpr int kMicroRunCap = 256;       // runs per warp in the global slab
+struct MicroCnt {
+  int n_runs, status;
+  int64_t key_lo, key_hi;
+};
+constexpr int kMicroBytes = (int)(((sizeof(MicroCnt) + 15) & ~15) + (kMicroRuns + 1) * 8 + kMicroElems * 8);
+
+static_assert(((sizeof(UnitSh) + 15) & ~size_t(15)) + kNW * kClassPts * 8 + (size_t)kNW * kMicroBytes <=
+                  (size_t)kSetsSmemBytes,
+              "micro tier does not fit the set kernel's shared memory");
+
+__device__ __forceinline__ void warp_bitonic(uint64_t* a, int p) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 2; k <= p; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < p; i += 32) {
+        const int l = i ^ j;
+        if (l > i) {
+          const uint64_t x = a[i], y = a[l];
+          const bool up = (i & k) == 0;
+          if ((x > y) == up) { a[i] = y; a[l] = x; }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// returns false when the unit must be processed by the whole CTA
+__device__ bool micro_unit(const SetsArgs& P, int64_t bidx, uint8_t* reg, int64_t* wpts, Run* wruns) {
+  const int lane = threadIdx.x & 31;
+  const int F = P.F_stride, S = P.S_req;
+  const int64_t c = bidx / ((int64_t)F * S);
+  const int f = (int)((bidx / S) % F);
+  const int j = (int)(bidx % S);
+  const Geo& G = P.geos[c];
+  const gvo_config cfg = P.cfgs[c];
+  const int tpl = cfg.template_id;
+  if (f >= P.T.n_fields[tpl] || !phase_ok(G, 0) || j >= G.n_samples || G.dup_of[f][j] >= 0) return true;
+  MicroCnt* cnt = reinterpret_cast<MicroCnt*>(reg);
+  int64_t* roff = reinterpret_cast<int64_t*>(reg + ((sizeof(MicroCnt) + 15) & ~size_t(15)));
+  uint64_t* el = reinterpret_cast<uint64_t*>(roff + kMicroRuns + 1);
+  const gvo_machine& mach = P.machines[cfg.machine_id];
+  const Granule Gr = Granule::make(mach.sector_bytes);
+  const int64_t R = mach.l1_line_bytes / mach.sector_bytes;
+  const int abase = P.T.acc_base[tpl];
+  const int64_t* fbase = P.T.field_base + P.T.field_base_off[tpl];
+  const int32_t bd[3] = {cfg.block[0], cfg.block[1], cfg.block[2]};
+  const int64_t gd[3] = {cfg.grid[0], cfg.grid[1], cfg.grid[2]};
+  const int64_t* crow = P.coefs + c * (int64_t)P.T.max_acc * 8;
+  const int64_t blk = G.sample_lin[j];
+  if (lane == 0) {
+    cnt->n_runs = 0;
+    cnt->status = GVO_OK;
+    cnt->key_lo = INT64_MAX;
+    cnt->key_hi = INT64_MIN;
+  }
+  __syncwarp();
+  RunSink sink{wruns, kMicroRunCap, &cnt->n_runs, &cnt->status, &cnt->key_lo, &cnt->key_hi};
+  const CTab ct{const_cast<int64_t*>(P.ctabs) + c * ctab_stride(P.T.max_acc), P.T.max_acc};
+  const int32_t* fko = P.T.fk_off + tpl * (2 * kMaxFields + 1);
+  Box box;
+  box.lo[0] = blk % gd[0]; box.lo[1] = (blk / gd[0]) % gd[1]; box.lo[2] = blk / (gd[0] * gd[1]);
+  box.n[0] = box.n[1] = box.n[2] = 1;
+  for (int kind = 0; kind < 2; ++kind) {
+    const int slot = f * 2 + kind;
+    // non-affine accesses: points runs
+    for (int q = fko[slot] + lane; q < fko[slot + 1]; q += 32) {
+      const int a = P.T.fk_list[q];
+      if (crow[a * 8 + 7] == kAffine) continue;
+      int64_t clo[6], chi[6];
+      clo[0] = clo[1] = clo[2] = 0;
+      chi[0] = bd[0] - 1; chi[1] = bd[1] - 1; chi[2] = bd[2] - 1;
+      run_bid_bounds(blk, 1, gd, clo + 3, chi + 3);
+      int64_t lo, hi;
+      bounds_check(P.T.code + P.T.code_off[abase + a], P.T.code_len[abase + a], clo, chi, bd, fbase, &lo, &hi);
+      const int sr = atomicAdd(&cnt->n_runs, 1);
+      if (sr >= kMicroRunCap) { atomicExch(&cnt->status, GVO_ERR_CAPACITY); continue; }
+      Run r;
+      r.kind = 1; r.access = a; r.tag = kind; r.run_start = blk; r.run_count = 1; r.count = G.tpb;
+      r.mono = 0; r.pieces = 1; r.nd = 0; r.base = 0; r.span = 0;
+      wruns[sr] = r;
+      atomicMin((long long*)&cnt->key_lo, (long long)Gr.of(lo));
+      atomicMax((long long*)&cnt->key_hi, (long long)Gr.of(hi));
+    }
+    // lattices per coefficient class
+    const int64_t cl0 = ct.slot_first()[slot], cl1 = ct.slot_first()[slot + 1];
+    for (int64_t cls = cl0; cls < cl1; ++cls) {
+      const int64_t* ca = crow + ct.rep()[cls] * 8;
+      const Lat L0 = box_lattice(ca, bd, box, Gr);
+      const int64_t* cp = ct.pts() + ct.start()[cls];
+      const int64_t np = ct.cnt()[cls];
+      for (int64_t p0 = 0; p0 < np; p0 += kClassPts) {
+        const int m = (int)((np - p0) < kClassPts ? (np - p0) : kClassPts);
+        __syncwarp();
+        for (int k = lane; k < m; k += 32) wpts[k] = (int64_t)((uint64_t)L0.base + (uint64_t)cp[p0 + k]);
+        __syncwarp();
+        cover_warp(sink, L0, wpts, m, kind, Gr);
+      }
+    }
+  }
+  __syncwarp();
+  const int nr = cnt->n_runs;
+  if (cnt->status != GVO_OK || nr > kMicroRuns) return false;
+  // offsets
+  if (lane == 0) {
+    int64_t acc = 0;
+    for (int r = 0; r < nr; ++r) { roff[r] = acc; acc += wruns[r].count; }
+    roff[nr] = acc;
+  }
+  __syncwarp();
+  const int64_t N = roff[nr];
+  const int64_t kbase = nr ? floordiv(cnt->key_lo, R) * R : 0;
+  if (N > kMicroElems || (nr && (uint64_t)(cnt->key_hi - kbase) >= (uint64_t(1) << kKeyBits))) return false;
+  int p = 32;
+  while (p < N) p <<= 1;
+  const int64_t tpb = G.tpb;
+  for (int64_t i = lane; i < p; i += 32) {
+    if (i >= N) { el[i] = ~0ull; continue; }
+    int lo = 0, hi = nr - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (roff[mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    const Run& rr = wruns[lo];
+    int64_t glo, ghi;
+    run_interval(rr, i - roff[lo], Gr, P.T, abase, fbase, bd, gd, tpb, &glo, &ghi);
+    el[i] = ((uint64_t)(glo - kbase) << kKeyShift) | ((uint64_t)(ghi - glo) << kTagBits) | (uint64_t)rr.tag;
+  }
+  __syncwarp();
+  warp_bitonic(el, p);
+  // sweep: loads (sectors), loads (lines), stores (sectors)
+  const uint32_t masks[3] = {1u, 1u, 2u};
+  const int64_t rs[3] = {1, R, 1};
+  int rsh = -1;
+  if ((R & (R - 1)) == 0) { rsh = 0; while ((int64_t(1) << rsh) < R) ++rsh; }
+  const int sub = p / 32;
+  const int lb = lane * sub;
+  int64_t res[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    int64_t mx = -1;
+    for (int i = lb; i < lb + sub && i < N; ++i) {
+      const uint64_t x = el[i];
+      if (!((masks[q] >> (x & 31u)) & 1u)) continue;
+      int64_t hi0 = (int64_t)(x >> kKeyShift) + (int64_t)((x >> kTagBits) & kLenMask);
+      if (rs[q] != 1) hi0 = rsh >= 0 ? hi0 >> rsh : hi0 / rs[q];
+      mx = max(mx, hi0);
+    }
+    int64_t inc = mx;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc = max(inc, t);
+    }
+    int64_t Rm = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) Rm = -1;
+    int64_t cntv = 0;
+    for (int i = lb; i < lb + sub && i < N; ++i) {
+      const uint64_t x = el[i];
+      if (!((masks[q] >> (x & 31u)) & 1u)) continue;
+      int64_t lo0 = (int64_t)(x >> kKeyShift);
+      int64_t hi0 = lo0 + (int64_t)((x >> kTagBits) & kLenMask);
+      if (rs[q] != 1) {
+        lo0 = rsh >= 0 ? lo0 >> rsh : lo0 / rs[q];
+        hi0 = rsh >= 0 ? hi0 >> rsh : hi0 / rs[q];
+      }
+      if (lo0 > Rm) cntv += hi0 - lo0 + 1;
+      else if (hi0 > Rm) cntv += hi0 - Rm;
+      Rm = max(Rm, hi0);
+    }
+    for (int o = 16; o; o >>= 1) cntv += __shfl_xor_sync(0xffffffffu, cntv, o);
+    res[q] = cntv;
+  }
+  if (lane == 0) {
+    int64_t* row = P.counts + c * P.counts_stride;
+    int64_t* b = row + GVO_C_HDR + ((int64_t)j * P.F_stride + f) * 5;
+    b[0] = res[0];
+    b[2] = res[1];
+    b[3] = res[2];
+  }
+  __syncwarp();
+  return true;
+}
+
 // Write a finished unit's measures (union counts per subset) to the outputs.
+template <class V>
 __device__ void write_unit_outputs(const SetsArgs& P, int64_t c, int field, int kind, int j, int n_uw,
-                                   const unsigned long long* v /* [n_sub] */) {
+                                   const V* v /* [n_sub] */) {
   const int f = field;
   if (P.mode == 0) {
     int64_t* row = P.counts + c * P.counts_stride;
@@ -619,11 +805,12 @@ __global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
   extern __shared__ __align__(16) uint8_t smem[];
   UnitSh& U = *reinterpret_cast<UnitSh*>(smem);
   size_t off = (sizeof(UnitSh) + 15) & ~size_t(15);
+  int64_t* cpts = reinterpret_cast<int64_t*>(smem + off); off += kNW * kClassPts * 8;
+  uint8_t* micro_region = smem + off;  // reused by the warp-per-unit tier
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + off); off += kNW * 256 * 4;
   uint32_t* tot = reinterpret_cast<uint32_t*>(smem + off); off += 256 * 4;
   int64_t* wmax = reinterpret_cast<int64_t*>(smem + off); off += kMaxSub * kNW * 8;
   int64_t* roff_sh = reinterpret_cast<int64_t*>(smem + off); off += (kSmemRuns + 1) * 8;
-  int64_t* cpts = reinterpret_cast<int64_t*>(smem + off); off += kNW * kClassPts * 8;
   int64_t* rka_sh = reinterpret_cast<int64_t*>(smem + off); off += kSmemRuns * 8;
   uint64_t* ebuf = reinterpret_cast<uint64_t*>(smem + off);
   const int64_t sm_elems = P.sm_cap > 0 ? min((int64_t)(kSetsSmemBytes - off) / 16, P.sm_cap)
@@ -640,8 +827,21 @@ __global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
   __shared__ int next_kind;  // 0 main item, 1 range item, 2 exit
   __shared__ RangeItem cur_range;
   __shared__ int main_done;
-  if (threadIdx.x == 0) main_done = 0;
-  const int64_t n_main = P.n_items + P.n_warp_items;
+  __shared__ int64_t fb_list[kNW];  // micro units that fell back to the CTA path
+  __shared__ int fb_n, fb_i;
+  __shared__ int64_t stat_idx;
+  __shared__ long long t_runs_sh;
+  if (threadIdx.x == 0) { main_done = 0; fb_n = 0; fb_i = 0; }
+  // item space (mode 0): wave units | bundles of kNW block units (micro) | warp items;
+  // block units falling back to the CTA path re-enter as kBlkBase + index
+  const bool micro_on = P.mode == 0 && P.S_req > 0;
+  const int64_t n_cfg_u = P.mode == 0 ? P.n_items / ((int64_t)P.F_stride * (P.S_req + 1)) : 0;
+  const int64_t n_wave_u = n_cfg_u * P.F_stride;
+  const int64_t n_blk_u = n_cfg_u * P.F_stride * P.S_req;
+  const int64_t n_bund = micro_on ? (n_blk_u + kNW - 1) / kNW : 0;
+  const int64_t n_set_main = micro_on ? n_wave_u + n_bund : P.n_items;
+  const int64_t n_main = n_set_main + P.n_warp_items;
+  const int64_t kBlkBase = int64_t(1) << 40;
 
   for (;;) {
     // ---------------- fetch: queued key ranges first, then main items
@@ -649,6 +849,13 @@ __global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
       int kind = 2;
       int64_t it = -1;
       for (;;) {
+        if (fb_i < fb_n) {
+          kind = 0;
+          it = kBlkBase + fb_list[fb_i++];
+          if (fb_i == fb_n) fb_i = fb_n = 0;
+          if (SS) atomicAdd(&SS->pending, 1ull);
+          break;
+        }
         if (SS) {
           const unsigned long long t = min(vload(&SS->qtail), (unsigned long long)SS->q_cap);
           const unsigned long long h = vload(&SS->qhead);
@@ -658,7 +865,12 @@ __global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
               while (*rd != P.epoch) __nanosleep(64);
               __threadfence();
               cur_range = SS->queue[h];
-              kind = 1;
+              if (cur_range.desc < 0) {  // a micro unit handed back to the CTA path
+                kind = 0;
+                it = kBlkBase + (-1 - cur_range.desc);
+              } else {
+                kind = 1;
+              }
               break;
             }
             continue;
@@ -691,9 +903,53 @@ __global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
     bool in_range = kind_fetched == 1;
     const long long t_start = clock64();
 
-    if (!in_range && item >= P.n_items) {
-      warp_item(P.warp, item - P.n_items, reinterpret_cast<unsigned long long*>(ebuf));
+    if (!in_range && item >= n_set_main && item < kBlkBase) {
+      warp_item(P.warp, item - n_set_main, reinterpret_cast<unsigned long long*>(ebuf));
       __syncthreads();
+      if (threadIdx.x == 0 && SS) atomicAdd(&SS->pending, ~0ull);
+      continue;
+    }
+    if (!in_range && micro_on && item >= n_wave_u && item < n_set_main) {
+      // bundle of kNW block units, one per warp
+      const int w = threadIdx.x >> 5;
+      const int64_t bidx = (item - n_wave_u) * kNW + w;
+      if (bidx < n_blk_u) {
+        const bool ok = micro_unit(P, bidx, micro_region + w * kMicroBytes, cpts + w * kClassPts,
+                                   runs + w * kMicroRunCap);
+        if (!ok && (threadIdx.x & 31) == 0) {
+          bool queued = false;
+          if (SS) {
+            atomicAdd(&SS->pending, 1ull);
+            const unsigned long long slot = atomicAdd(&SS->qtail, 1ull);
+            if ((int64_t)slot < SS->q_cap) {
+              RangeItem it;
+              it.desc = -1 - bidx;
+              it.a = it.b = 0;
+              it.ready = 0;
+              it.pad = 0;
+              SS->queue[slot] = it;
+              __threadfence();
+              *reinterpret_cast<volatile int32_t*>(&SS->queue[slot].ready) = P.epoch;
+              queued = true;
+            } else {
+              atomicAdd(&SS->pending, ~0ull);
+            }
+          }
+          if (!queued) fb_list[atomicAdd(&fb_n, 1)] = bidx;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0 && P.unit_stats && SS) {
+        const unsigned long long slot =
+            atomicAdd(reinterpret_cast<unsigned long long*>(P.unit_stats + P.n_items * 10), 1ull);
+        if (slot < 4096) {
+          int64_t* us = P.unit_stats + P.n_items * 10 + 10 + slot * 10;
+          us[0] = -1; us[1] = item; us[2] = fb_n; us[3] = 0; us[4] = clock64() - t_start; us[5] = 0;
+          unsigned smid;
+          asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+          us[6] = smid; us[7] = 0; us[8] = 3;
+        }
+      }
       if (threadIdx.x == 0 && SS) atomicAdd(&SS->pending, ~0ull);
       continue;
     }
@@ -711,21 +967,22 @@ __global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
         int j = 0;
         bool skip = false;
         if (P.mode == 0) {
-          const int64_t n_cfg = P.n_items / ((int64_t)P.F_stride * (P.S_req + 1));
-          const int64_t n_wave = n_cfg * P.F_stride;
-          if (item < n_wave) {
+          if (item < n_wave_u) {
             c = item / P.F_stride;
             f = item % P.F_stride;
             j = P.S_req;
+            stat_idx = item;
           } else {
-            const int64_t r = item - n_wave;
+            const int64_t r = item >= kBlkBase ? item - kBlkBase : item - n_wave_u;
             c = r / ((int64_t)P.F_stride * P.S_req);
             f = (r / P.S_req) % P.F_stride;
             j = (int)(r % P.S_req);
+            stat_idx = n_wave_u + r;
           }
         } else {
           c = 0;
           f = item;
+          stat_idx = item;
         }
         const Geo& G = P.geos[c];
         const gvo_config& cfg = P.cfgs[c];
@@ -894,13 +1151,31 @@ __global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
       }
       __syncthreads();
 
+    if (threadIdx.x == 0) t_runs_sh = clock64();
     // ---------------- offsets of runs, element count
       const int nr = min(U.n_runs, (int)P.run_cap);
       int64_t* roff = nr <= kSmemRuns ? roff_sh : roff_gl;
+      // run counts loaded in parallel, exclusive scan by warp 0
+      for (int r = threadIdx.x; r < nr; r += kNT) roff[r] = runs[r].count;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        int64_t carry = 0;
+        for (int r0 = 0; r0 < nr; r0 += 32) {
+          const int r = r0 + (int)threadIdx.x;
+          const int64_t v = r < nr ? roff[r] : 0;
+          int64_t inc = v;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if ((int)threadIdx.x >= o) inc += t;
+          }
+          if (r < nr) roff[r] = carry + inc - v;
+          carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (threadIdx.x == 0) roff[nr] = carry;
+      }
+      __syncthreads();
       if (threadIdx.x == 0) {
-        int64_t acc = 0;
-        for (int r = 0; r < nr; ++r) { roff[r] = acc; acc += runs[r].count; }
-        roff[nr] = acc;
+        const int64_t acc = roff[nr];
         U.N = acc;
         const int64_t base = floordiv(U.key_lo, U.R) * U.R;
         U.key_lo = base;
@@ -1155,9 +1430,8 @@ __global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
               atomicExch(P.status_out, hdr->status);
             }
           } else {
-            unsigned long long v[kMaxSubC];
-            for (int q = 0; q < hdr->n_sub; ++q) v[q] = vload(&hdr->acc[q]);
-            write_unit_outputs(P, c, hdr->field, hdr->kind, hdr->j, hdr->n_uw, v);
+            write_unit_outputs(P, c, hdr->field, hdr->kind, hdr->j, hdr->n_uw,
+                               reinterpret_cast<const volatile unsigned long long*>(hdr->acc));
           }
         }
         atomicAdd(&SS->pending, ~0ull);
@@ -1180,7 +1454,7 @@ __global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
       const int64_t tpb = G.tpb;
       const int nr = min(U.n_runs, (int)P.run_cap);
       int64_t* roff = nr <= kSmemRuns ? roff_sh : roff_gl;
-      const long long t_runs = t_start;
+      const long long t_runs = t_runs_sh;
     const int64_t N = U.N;
       uint64_t* A0;
       uint64_t* B0;
@@ -1270,7 +1544,7 @@ __global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
 
       // ---------------- outputs
       if (threadIdx.x == 0 && P.unit_stats) {
-        int64_t* us = P.unit_stats + item * 10;
+        int64_t* us = P.unit_stats + stat_idx * 10;
         us[6] = t_runs - t_start;
         us[7] = t_emit - t_runs;
         us[8] = t_sort - t_emit;
@@ -1285,9 +1559,7 @@ __global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
         us[5] = smid;
       }
       if (threadIdx.x == 0) {
-        unsigned long long v[kMaxSubC];
-        for (int q = 0; q < U.n_sub; ++q) v[q] = (unsigned long long)U.sub_val[q];
-        write_unit_outputs(P, c, U.field, U.kind, U.j, P.mode == 2 ? 0 : G.n_uw, v);
+        write_unit_outputs(P, c, U.field, U.kind, U.j, P.mode == 2 ? 0 : G.n_uw, U.sub_val);
         if (SS) atomicAdd(&SS->pending, ~0ull);
       }
       __syncthreads();

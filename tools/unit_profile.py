@@ -46,6 +46,10 @@ for name, grp in (("wave", wave), ("block", blk)):
 json.dump(rows, open(ROOT / "gpurun_out" / "unit_profile.json", "w"))
 print("ranges processed", nrng)
 if nrng:
-    rr = sorted(rng_rows.tolist(), key=lambda r: -r[4])
+    bund = [r for r in rng_rows.tolist() if r[8] == 3]
+    if bund:
+        cyc = sorted(r[4] for r in bund)
+        print("bundles", len(bund), "total Mcycles", sum(cyc) / 1e6, "p50", cyc[len(cyc)//2], "max", cyc[-1], "fallbacks", sum(r[2] for r in bund))
+    rr = sorted([r for r in rng_rows.tolist() if r[8] != 3], key=lambda r: -r[4])
     print("range cycles total M", sum(r[4] for r in rr) / 1e6, "max", rr[0][4])
     for r in rr[:15]: print("desc", r[0], "a", r[1], "b", r[2], "N", r[3], "cyc", r[4], "nr", r[5], "sm", r[6], "cfg", kept[r[7]].key, "queued" if r[8] == 1 else "first")
