@@ -33,9 +33,9 @@ sys.path.insert(0, str(ROOT))
 
 GRID = (640, 640, 640)
 RADIUS = 4
-# kernels per step: setup, warp stats, interval sets, assembly (one batch)
-# + rank: keys, 2 x 8 digit passes x (hist, scan, scatter), gather, output
-LAUNCHES_PER_STEP = 4 + 1 + 48 + 1 + 1
+# kernels per step (one batch): k_setup, k_sets (warp statistics fused),
+# k_finish, k_rank_small (n <= 2048)
+LAUNCHES_PER_STEP = 4
 
 
 def sweep_configs():
@@ -141,18 +141,27 @@ def cpu_sample_rate(configs_for_cpu, seconds_target=20.0):
     import multiprocessing as mp
 
     cores = len(os.sched_getaffinity(0))
-    n = max(cores, 8)
+    n = max(3 * cores, 24)
     rng = np.random.default_rng(20240811)
     pick = [configs_for_cpu[i] for i in rng.choice(len(configs_for_cpu), size=min(n, len(configs_for_cpu)),
                                                      replace=False)]
     kind = _ref_kind()
     t0 = time.perf_counter()
     with mp.get_context("spawn").Pool(min(cores, len(pick))) as pool:
-        pool.map(_cpu_eval, [(kind, c) for c in pick])
-    dt = time.perf_counter() - t0
+        pool.map(_warm, range(min(cores, len(pick))))  # imports outside the timed sample
+        t0 = time.perf_counter()
+        list(pool.imap_unordered(_cpu_eval, [(kind, c) for c in pick], chunksize=1))
+        dt = time.perf_counter() - t0
     return {"value": len(pick) / dt, "unit": "configs/s", "cores": min(cores, len(pick)), "kind": kind,
             "sample": f"{len(pick)} seeded-random configs of the 246-config C2 sweep, "
                       f"reference evaluate_kernel (B200 params, samples 5/2), {dt:.1f} s"}
+
+
+def _warm(_):
+    if (ROOT / "baseline" / "_ref" / "gvo").exists():
+        sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
+        import gvo  # noqa: F401
+    return 0
 
 
 def _ref_kind():
@@ -320,7 +329,7 @@ def run_device(args, rank, world):
                    "configs_per_rank": n, "parallelism": f"dp{world} (config shards, NCCL all-gather + device rank)",
                    "l2": "flushed between timed steps (256 MiB write)"},
         "e2e": {"value": e2e_value, "unit": "configs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": int(args.steps * LAUNCHES_PER_STEP),
+        "gpu_launches": int(sum(kcnt[i] for i in range(5))),
         "kernel_ms_per_step": kernel_ms,
         "roofline": {"bound": "int", "kernel": "k_sets (interval-union engine)",
                      "achieved": achieved, "peak": peak.value / 1e9, "unit": "Gop/s (int32, address-equivalent)",
@@ -330,7 +339,7 @@ def run_device(args, rank, world):
                              "than enumeration. peak = measured INT32 issue rate (gvo_int_peak).",
                      "hbm": {"achieved": algo_bytes / (ms_step * 1e-3) / 1e9, "peak": 6531.3, "unit": "GB/s",
                              "frac": algo_bytes / (ms_step * 1e-3) / 1e9 / 6531.3},
-                     "traffic": None},
+                     "traffic": _ncu_traffic()},
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }
@@ -346,13 +355,14 @@ def run_reference(args, rank, world):
     keys = [c.key for c in _valid_cfgs()]
     kind = _ref_kind()
     rng = np.random.default_rng(20240811)
-    per_step = max(cores, 8)
+    per_step = max(3 * cores, 24)
     times = []
     with mp.get_context("spawn").Pool(cores) as pool:
+        pool.map(_warm, range(cores))
         for i in range(args.warmup + args.steps):
             pick = [keys[j] for j in rng.choice(len(keys), size=min(per_step, len(keys)), replace=False)]
             t0 = time.perf_counter()
-            pool.map(_cpu_eval, [(kind, k) for k in pick])
+            list(pool.imap_unordered(_cpu_eval, [(kind, k) for k in pick], chunksize=1))
             if i >= args.warmup:
                 times.append((len(pick), time.perf_counter() - t0))
     n_done = sum(a for a, _ in times)
@@ -371,6 +381,21 @@ def run_reference(args, rank, world):
         "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _ncu_traffic():
+    """dram read+write bytes per k_sets launch from the committed ncu capture
+    (profiles/r01_ncu_k_sets.json), or None."""
+    p = ROOT / "profiles" / "r01_ncu_k_sets.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = 0.0
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        v, u = d[k]
+        tot += float(v) * scale.get(u, 1)
+    return tot
 
 
 def _valid_cfgs():

@@ -163,7 +163,7 @@ int gvo_open(int device, gvo_ctx** out) {
   if (const char* e = getenv("GVO_RUN_CAP")) ctx->run_cap = atoll(e);
   if (const char* e = getenv("GVO_BATCH")) ctx->batch = atoll(e);
   if (const char* e = getenv("GVO_SMEM_ELEMS")) ctx->sm_cap = atoll(e);
-  ctx->n_ctas = 2 * ctx->n_sm;
+  ctx->n_ctas = kSetsCtasPerSm * ctx->n_sm;
   *out = ctx;
   return GVO_OK;
 }

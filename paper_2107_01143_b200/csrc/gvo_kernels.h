@@ -6,8 +6,12 @@
 
 namespace gvo {
 
-// dynamic shared memory of the set kernel (2 CTAs per SM)
-constexpr int kSetsSmemBytes = 110 * 1024;
+// set kernel residency: CTAs per SM and dynamic shared memory per CTA
+#ifndef GVO_SETS_CTAS_PER_SM
+#define GVO_SETS_CTAS_PER_SM 2
+#endif
+constexpr int kSetsCtasPerSm = GVO_SETS_CTAS_PER_SM;
+constexpr int kSetsSmemBytes = kSetsCtasPerSm == 1 ? 222 * 1024 : 110 * 1024;
 
 void launch_setup(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs,
                   int64_t n, const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos, int64_t* d_ctabs,

@@ -801,7 +801,7 @@ __device__ __forceinline__ unsigned long long vload(const unsigned long long* p)
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
-__global__ void __launch_bounds__(kNT, 2) k_sets(SetsArgs P) {
+__global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
   extern __shared__ __align__(16) uint8_t smem[];
   UnitSh& U = *reinterpret_cast<UnitSh*>(smem);
   size_t off = (sizeof(UnitSh) + 15) & ~size_t(15);
