@@ -10,6 +10,11 @@ its own 246-config shard (the same sweep with field alignment 8*rank bytes,
 so every rank's configs are distinct), records are all-gathered over NCCL
 and the global ranking runs on the device (weak scaling).
 
+--workload C1|C3|C4|C5 runs the other BASELINE.json configuration spaces
+(paper_2107_01143_b200/workloads.py): the space is dealt to ranks by
+estimated cost (shard.py), one NCCL all-gather of the records, device rank
+of the whole space (strong scaling: total work fixed).
+
 --impl reference times the reference's own CPU estimator (pip-installed
 unmodified under baseline/_ref; the CPU oracle port if that is missing) on a
 bounded sample of the same workload with all host cores.
@@ -38,17 +43,6 @@ RADIUS = 4
 LAUNCHES_PER_STEP = 4
 
 
-def sweep_configs():
-    from paper_2107_01143_b200 import gvo
-
-    out = []
-    t = 1
-    while t <= 1024:
-        out.extend(gvo.enumerate_sweep(t))
-        t *= 2
-    return out
-
-
 def b200_machine():
     from paper_2107_01143_b200 import gvo
 
@@ -56,43 +50,51 @@ def b200_machine():
 
 
 # ---------------------------------------------------------------- device arm
-def build_shard(rank: int):
-    """Device config records of this rank's shard + template bookkeeping."""
-    from dataclasses import replace
+WORKLOADS = {
+    "C1": "C1: 2D5pt Jacobi 256^2, block 32x4x1 (PR1 oracle config)",
+    "C2": "C2: 3D25pt r4 640^3 full power-of-two block sweep (246 valid configs/rank), "
+          "B200 machine params, samples 5/2, evaluate+rank",
+    "C3": "C3: 3D25pt/13pt (r4/r2) 640^3 x folding x layout fzyx/zyxf x 2/4 components x 16 alignments "
+          "(93,184 configs), B200 params, samples 5/2, evaluate+rank",
+    "C4": "C4: two-phase LBM 256^3 (D3Q27 hydro + D3Q15 phase field) x 154 blocks x folding x layout "
+          "(1,812 configs), B200 params, samples 5/2, evaluate+rank",
+    "C5": "C5: C3 (r1-4, 32 alignments) + C4 (16 alignments) x L2 capacity {1, 1/2, 1/4} "
+          "(1,205,184 configs), B200 params, samples 5/2, evaluate+rank",
+}
 
-    from paper_2107_01143_b200 import gvo
-    from paper_2107_01143_b200.gvo import _engine
 
-    fam = gvo.KernelFamily("stencil", GRID, radius=RADIUS)
+def build_shard(workload: str, rank: int, world: int):
+    """(Space of this rank's shard, padded shard length m, real configs of
+    the whole job).  C2: every rank evaluates its own 246-config sweep
+    (alignment 8*rank; weak scaling).  Others: the space is dealt by cost
+    and padded to equal length for the all-gather (strong scaling)."""
+    from paper_2107_01143_b200 import shard, workloads as W
+
     m = b200_machine()
-    batch = _engine.Batch()
-    kept = []
-    base = None
-    for cfg in sweep_configs():
-        try:
-            launch, flops = fam.launch_of(cfg)
-        except ValueError:
-            continue
-        if base is None:
-            k = fam.build(cfg)
-            fields = tuple(replace(f, alignment=8 * rank) for f in k.fields)
-            base = (fields, k.accesses)
-        batch.add(base[0], base[1], launch, flops, m, None, _engine.FOLD_RANK[cfg.folding])
-        kept.append(cfg)
-    return batch, kept
+    if workload == "C2":
+        sp = W.space_c2(m, GRID, RADIUS, alignment=8 * rank)
+        return sp, len(sp), len(sp) * world
+    sp = W.space(workload, m)
+    idx = shard.shard_indices(shard.config_cost(sp.block, sp.n_accesses()), world, rank)
+    mlen = shard.pad_to(len(sp), world)
+    if len(idx) < mlen:  # pad with this shard's own configs (evaluated, not counted)
+        idx = np.concatenate([idx, idx[: mlen - len(idx)]])
+    return sp.subset(idx), mlen, len(sp)
 
 
-def n_addr(cfg_launch, n_acc: int, m) -> int:
-    """Brute-force address-granule evaluations the reference performs for one
-    config: blocks n_b*T*A (+ lines), L1 T*A, waves U*B_w*T*A."""
-    t = cfg_launch.threads_per_block
-    per_sm = min(m.max_blocks_per_sm, m.max_threads_per_sm // t)
+def n_addr(sp, m) -> int:
+    """Brute-force address-granule evaluations the reference performs for the
+    configs of a space: blocks n_b*T*A (+ lines), L1 T*A,
+    waves U*B_w*T*A."""
+    t = sp.block.astype(np.int64).prod(axis=1)
+    per_sm = np.minimum(m.max_blocks_per_sm, m.max_threads_per_sm // t)
     bw = m.sm_count * per_sm
-    total = cfg_launch.total_blocks
+    total = sp.grid_dim.prod(axis=1)
     nw = -(-total // bw)
-    u = 1 if nw == 1 else 3
-    n_b = min(5, max(1, (cfg_launch.grid_dim[0] - 2) * (cfg_launch.grid_dim[1] - 2) * (cfg_launch.grid_dim[2] - 2)))
-    return n_b * t * n_acc + t * n_acc + u * min(bw, total) * t * n_acc
+    u = np.where(nw == 1, 1, 3)
+    n_b = np.minimum(5, np.maximum(1, np.clip(sp.grid_dim - 2, 1, None).prod(axis=1)))
+    a = sp.n_accesses()
+    return int((n_b * t * a + t * a + u * np.minimum(bw, total) * t * a).sum())
 
 
 class ClockSampler:
@@ -136,24 +138,29 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def cpu_sample_rate(configs_for_cpu, seconds_target=20.0):
+def cpu_jobs(sp, n, rng):
+    """n seeded-random (kind, spec dict, machine dict) jobs of a space."""
+    from paper_2107_01143_b200.gvo.kernels import kernel_to_dict
+    from paper_2107_01143_b200.gvo.machine import machine_to_dict
+
+    kind = _ref_kind()
+    pick = rng.choice(len(sp), size=min(n, len(sp)), replace=False)
+    return [(kind, kernel_to_dict(sp.kernel(int(i))), machine_to_dict(sp.machine(int(i)))) for i in pick]
+
+
+def cpu_sample_rate(sp, workload):
     """Reference CPU estimator on a bounded sample (multiprocessing pool)."""
     import multiprocessing as mp
 
     cores = len(os.sched_getaffinity(0))
-    n = max(3 * cores, 24)
-    rng = np.random.default_rng(20240811)
-    pick = [configs_for_cpu[i] for i in rng.choice(len(configs_for_cpu), size=min(n, len(configs_for_cpu)),
-                                                     replace=False)]
-    kind = _ref_kind()
-    t0 = time.perf_counter()
-    with mp.get_context("spawn").Pool(min(cores, len(pick))) as pool:
-        pool.map(_warm, range(min(cores, len(pick))))  # imports outside the timed sample
+    jobs = cpu_jobs(sp, max(3 * cores, 24), np.random.default_rng(20240811))
+    with mp.get_context("spawn").Pool(min(cores, len(jobs))) as pool:
+        pool.map(_warm, range(min(cores, len(jobs))))  # imports outside the timed sample
         t0 = time.perf_counter()
-        list(pool.imap_unordered(_cpu_eval, [(kind, c) for c in pick], chunksize=1))
+        list(pool.imap_unordered(_cpu_eval, jobs, chunksize=1))
         dt = time.perf_counter() - t0
-    return {"value": len(pick) / dt, "unit": "configs/s", "cores": min(cores, len(pick)), "kind": kind,
-            "sample": f"{len(pick)} seeded-random configs of the 246-config C2 sweep, "
+    return {"value": len(jobs) / dt, "unit": "configs/s", "cores": min(cores, len(jobs)), "kind": jobs[0][0],
+            "sample": f"{len(jobs)} seeded-random configs of the {workload} space, "
                       f"reference evaluate_kernel (B200 params, samples 5/2), {dt:.1f} s"}
 
 
@@ -169,24 +176,20 @@ def _ref_kind():
 
 
 def _cpu_eval(arg):
-    kind, key = arg
-    bx, by, bz = (int(v) for v in key.split("/")[0].split("x"))
+    """One configuration through the reference's public API (kernel spec +
+    machine JSON, as its CLI/bindings take them), or the oracle port."""
+    kind, spec, mdict = arg
     if kind == "reference":
         sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
-        import dataclasses
-
         import gvo as ref
+        from gvo.machine import machine_from_dict as ref_machine
 
-        m = dataclasses.replace(ref.v100_preset(), name="b200", sm_count=148, clock_ghz=1.965,
-                                l1_capacity_bytes=256 * 1024, l2_capacity_bytes=126 * 1024 * 1024,
-                                mem_bandwidth_gbps=6531.3, l2_bandwidth_gbps=20000.0)
-        k = ref.KernelFamily("stencil", GRID, radius=RADIUS).build(ref.SweepConfig((bx, by, bz)))
-        return ref.evaluate_kernel(k, m).glups
+        return ref.evaluate_kernel(ref.kernel_from_dict(spec), ref_machine(mdict)).glups
     from oracle import gvo_oracle as ora
     from paper_2107_01143_b200 import gvo
+    from paper_2107_01143_b200.gvo.machine import machine_from_dict
 
-    k = gvo.KernelFamily("stencil", GRID, radius=RADIUS).build(gvo.SweepConfig((bx, by, bz)))
-    return ora.evaluate_kernel(k, b200_machine())["glups"]
+    return ora.evaluate_kernel(gvo.kernel_from_dict(spec), machine_from_dict(mdict))["glups"]
 
 
 def run_device(args, rank, world):
@@ -199,9 +202,8 @@ def run_device(args, rank, world):
     torch.cuda.set_device(dev)
     ctx = _native.context()
     L = _native.lib()
-    batch, kept = build_shard(rank)
-    cfg_np = batch.config_array()
-    n = len(cfg_np)
+    sp, n, n_real = build_shard(args.workload, rank, world)
+    cfg_np = sp.config_array(ctx)
     ctx.sync_registries()
     F = ctx.max_fields
     S, W = _native.effective_sampling(5, 2)
@@ -218,20 +220,20 @@ def run_device(args, rank, world):
         dist.all_gather_into_tensor(g_cfgs, d_cfgs)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    sp = stream.cuda_stream
+    sptr = stream.cuda_stream
     C = _native.C
 
     def step():
         ctx.check(L.gvo_eval_configs(ctx.h, C.c_void_p(d_cfgs.data_ptr()), n, C.byref(smp), F,
                                      C.c_void_p(d_counts.data_ptr()), C.c_void_p(d_stats.data_ptr()),
-                                     C.c_void_p(d_rec.data_ptr()), None, None, 0, C.c_void_p(sp)))
+                                     C.c_void_p(d_rec.data_ptr()), None, None, 0, C.c_void_p(sptr)))
         if world > 1:
             dist.all_gather_into_tensor(g_rec, d_rec)
             ctx.check(L.gvo_rank(ctx.h, C.c_void_p(g_rec.data_ptr()), C.c_void_p(g_cfgs.data_ptr()), n * world,
-                                 C.c_void_p(d_order.data_ptr()), C.c_void_p(sp)))
+                                 C.c_void_p(d_order.data_ptr()), C.c_void_p(sptr)))
         else:
             ctx.check(L.gvo_rank(ctx.h, C.c_void_p(d_rec.data_ptr()), C.c_void_p(d_cfgs.data_ptr()), n,
-                                 C.c_void_p(d_order.data_ptr()), C.c_void_p(sp)))
+                                 C.c_void_p(d_order.data_ptr()), C.c_void_p(sptr)))
 
     for _ in range(args.warmup):
         step()
@@ -264,7 +266,7 @@ def run_device(args, rank, world):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     ms_step = ms_max / args.steps
-    value = n * world * args.steps / (ms_max * 1e-3)
+    value = n_real * args.steps / (ms_max * 1e-3)
 
     # ---- e2e through the C ABI with host buffers (copies inside the region)
     counts_h = np.zeros((n, stride), dtype=np.int64)
@@ -282,17 +284,17 @@ def run_device(args, rank, world):
         if world > 1:
             dist.all_gather_into_tensor(g_rec, rec_d)
             ctx.check(L.gvo_rank(ctx.h, C.c_void_p(g_rec.data_ptr()), C.c_void_p(g_cfgs.data_ptr()), n * world,
-                                 C.c_void_p(d_order.data_ptr()), C.c_void_p(sp)))
+                                 C.c_void_p(d_order.data_ptr()), C.c_void_p(sptr)))
         else:
             ctx.check(L.gvo_rank(ctx.h, C.c_void_p(rec_d.data_ptr()), C.c_void_p(d_cfgs.data_ptr()), n,
-                                 C.c_void_p(d_order.data_ptr()), C.c_void_p(sp)))
+                                 C.c_void_p(d_order.data_ptr()), C.c_void_p(sptr)))
         order_h = d_order.cpu().numpy()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = n * world * e2e_steps / float(te.item())
+    e2e_value = n_real * e2e_steps / float(te.item())
     h2d = n * cfg_np.itemsize + n * _native.RECORD_LEN * 8
     d2h = n * stride * 8 + n * _native.stats_len(F) * 8 + n * _native.RECORD_LEN * 8 + n * world * 8
     del order_h
@@ -305,27 +307,19 @@ def run_device(args, rank, world):
     top = max(("setup", "warp", "sets", "finish"), key=lambda k: kernel_ms[k])
     peak = C.c_double()
     ctx.check(L.gvo_int_peak(ctx.h, C.byref(peak)))
-    m = b200_machine()
-    fam_acc = 26
-    n_addr_total = 0
-    from paper_2107_01143_b200 import gvo as G
-
-    fam = G.KernelFamily("stencil", GRID, radius=RADIUS)
-    for cfg in kept:
-        launch, _ = fam.launch_of(cfg)
-        n_addr_total += n_addr(launch, fam_acc, m)
+    n_addr_total = n_addr(sp, b200_machine())
     k_int = 8
     sets_s = kernel_ms["sets"] * 1e-3
     achieved = k_int * n_addr_total / sets_s / 1e9
     algo_bytes = n * (cfg_np.itemsize + stride * 8 + _native.stats_len(F) * 8 + _native.RECORD_LEN * 8)
-    cpu = cpu_sample_rate([c.key for c in kept]) if world == 1 and not args.no_cpu else None
+    cpu = cpu_sample_rate(sp, args.workload) if world == 1 and not args.no_cpu else None
     line = {
         "metric": "kernel configs evaluated/sec (1/2/4/8 B200) vs host-CPU reference; % int/HBM roofline",
         "value": value, "unit": "configs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak" if args.workload == "C2" else "strong", "vs_baseline": None,
         "dtype": "int64", "data": "synthetic (deterministic config-space enumeration)",
-        "config": {"workload": "C2: 3D25pt r4 640^3 full power-of-two block sweep (246 valid configs/rank), "
-                               "B200 machine params, samples 5/2, evaluate+rank",
+        "config": {"workload": WORKLOADS[args.workload], "configs_total": n_real,
                    "configs_per_rank": n, "parallelism": f"dp{world} (config shards, NCCL all-gather + device rank)",
                    "l2": "flushed between timed steps (256 MiB write)"},
         "e2e": {"value": e2e_value, "unit": "configs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -347,24 +341,28 @@ def run_device(args, rank, world):
 
 
 def run_reference(args, rank, world):
+    """The reference's own CPU estimator on bounded samples of the workload,
+    all host cores (rank 0 only under torchrun)."""
     if rank != 0:
         return
     import multiprocessing as mp
 
+    from paper_2107_01143_b200 import workloads as W
+
     cores = len(os.sched_getaffinity(0))
-    keys = [c.key for c in _valid_cfgs()]
-    kind = _ref_kind()
+    sp = W.space_c2(b200_machine(), GRID, RADIUS) if args.workload == "C2" else W.space(args.workload)
     rng = np.random.default_rng(20240811)
     per_step = max(3 * cores, 24)
     times = []
+    kind = _ref_kind()
     with mp.get_context("spawn").Pool(cores) as pool:
         pool.map(_warm, range(cores))
         for i in range(args.warmup + args.steps):
-            pick = [keys[j] for j in rng.choice(len(keys), size=min(per_step, len(keys)), replace=False)]
+            jobs = cpu_jobs(sp, per_step, rng)
             t0 = time.perf_counter()
-            list(pool.imap_unordered(_cpu_eval, [(kind, k) for k in pick], chunksize=1))
+            list(pool.imap_unordered(_cpu_eval, jobs, chunksize=1))
             if i >= args.warmup:
-                times.append((len(pick), time.perf_counter() - t0))
+                times.append((len(jobs), time.perf_counter() - t0))
     n_done = sum(a for a, _ in times)
     secs = sum(b for _, b in times)
     value = n_done / secs
@@ -372,12 +370,13 @@ def run_reference(args, rank, world):
         "impl": "reference",
         "metric": "kernel configs evaluated/sec (1/2/4/8 B200) vs host-CPU reference; % int/HBM roofline",
         "value": value, "unit": "configs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": secs / len(times) * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": secs / len(times) * 1e3, "higher_is_better": True,
+        "scaling": "weak" if args.workload == "C2" else "strong", "vs_baseline": None,
         "dtype": "int64", "data": "synthetic (deterministic config-space enumeration)",
-        "config": {"workload": "C2: 3D25pt r4 640^3 full power-of-two block sweep, B200 params, samples 5/2",
-                   "per_step_sample": per_step},
+        "config": {"workload": WORKLOADS[args.workload], "per_step_sample": per_step},
         "cpu_baseline": {"value": value, "unit": "configs/s", "cores": cores, "kind": kind,
-                         "sample": f"{per_step} seeded-random configs per step of the 246-config sweep"},
+                         "sample": f"{per_step} seeded-random configs per step of the {args.workload} space, "
+                                   "unmodified reference evaluate_kernel"},
         "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -398,20 +397,6 @@ def _ncu_traffic():
     return tot
 
 
-def _valid_cfgs():
-    from paper_2107_01143_b200 import gvo
-
-    fam = gvo.KernelFamily("stencil", GRID, radius=RADIUS)
-    out = []
-    for c in sweep_configs():
-        try:
-            fam.launch_of(c)
-            out.append(c)
-        except ValueError:
-            pass
-    return out
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -419,6 +404,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--no-cpu", action="store_true", help="skip the in-run CPU baseline")
+    ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
