@@ -290,6 +290,20 @@ int gvo_predict_host(gvo_ctx* ctx, const int32_t* h_machine_id, const double* h_
                      const double* h_l2_down, const double* h_cycles_per_lup,
                      const int64_t* h_flops, int64_t n, double* h_out);
 
+/* ---- ranking CSV (host) ----
+ * Rows of render_ranking_csv (reference report.py:242-255, columns of
+ * RANKING_CSV_COLUMNS report.py:162-205): for r in 0..n-1, config
+ * i = order[r] (i = r when order is NULL): the caller's text prefix i
+ * (prefixes[prefix_off[i] .. prefix_off[i+1]), i.e. "configKey,blockX,
+ * blockY,blockZ,folding"), then the 37 record columns, each formatted as
+ * Python format(v, ".10g") (NaN coverage = None -> empty cell), the
+ * limiter by name, '\n' per row.  Pure host code, n_threads workers
+ * (<= 0: all cores).  *len_out = bytes needed; GVO_ERR_CAPACITY when out is
+ * NULL or cap is smaller (nothing written). */
+int gvo_format_ranking_csv(const double* h_records, int64_t n, const int64_t* h_order,
+                           const char* prefixes, const int64_t* prefix_off, int32_t n_threads,
+                           char* out, int64_t cap, int64_t* len_out);
+
 /* ---- instrumentation ---- */
 /* Enable CUDA-event timing around every pipeline kernel (on the stream the
  * kernel is launched on). */

@@ -26,6 +26,7 @@ C_STATUS, C_ERR_PHASE, C_ERR_GROUP, C_ERR_ACCESS = 0, 1, 2, 3
 C_NSAMPLES, C_NUWAVES, C_NPAIRS, C_HASPRED = 4, 5, 6, 7
 C_PERWAVE, C_NWAVES, C_L1BLOCK, C_L1CYCLES, C_FIRSTWAVE, C_FIRSTBLOCK = 8, 9, 10, 11, 12, 13
 
+STATUS_CAPACITY = 7
 STATUS = {0: "OK", 1: "EXPR", 2: "ADDRESS_OVERFLOW", 3: "KERNEL", 4: "FOOTPRINT", 5: "MACHINE",
           6: "PERF", 7: "CAPACITY", 8: "UNSUPPORTED", 15: "INVALID", 16: "CUDA", 17: "NCCL"}
 
@@ -150,6 +151,7 @@ def lib():
             "gvo_kernel_times": (C.c_int, [P, P, P, C.c_int]),
             "gvo_int_peak": (C.c_int, [P, C.POINTER(C.c_double)]),
             "gvo_debug_units": (C.c_int, [P, C.c_int, P, i64, C.POINTER(C.c_int64)]),
+            "gvo_format_ranking_csv": (C.c_int, [P, i64, P, C.c_char_p, P, i32, P, i64, C.POINTER(C.c_int64)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -166,7 +168,7 @@ EXPORTED_SYMBOLS = (
     "gvo_set_machines", "gvo_counts_stride_eff", "gvo_eval_configs", "gvo_eval_configs_host",
     "gvo_rank", "gvo_group_footprint", "gvo_group_sets", "gvo_l1_cycles", "gvo_eval_addresses",
     "gvo_assemble_host", "gvo_predict_host", "gvo_set_timing", "gvo_kernel_times", "gvo_int_peak",
-    "gvo_debug_units",
+    "gvo_debug_units", "gvo_format_ranking_csv",
 )
 
 
@@ -513,3 +515,29 @@ def rank_host(cfgs: np.ndarray, records: np.ndarray) -> np.ndarray:
     stream = torch.cuda.current_stream(dev)
     rank_device(rec.data_ptr(), cf.data_ptr(), n, order.data_ptr(), stream.cuda_stream)
     return order.cpu().numpy()
+
+
+def format_ranking_csv(records: np.ndarray, prefixes: list[str], order=None, n_threads: int = 0) -> str:
+    """Ranking CSV body rows (no header) via the native formatter; byte-identical
+    to the reference's render_ranking_csv rows (report.py:242-255)."""
+    rec = np.ascontiguousarray(records, dtype=np.float64).reshape(-1, RECORD_LEN)
+    n = len(rec)
+    if len(prefixes) != n:
+        raise ValueError("one prefix per record")
+    enc = [p.encode() for p in prefixes]
+    off = np.zeros(n + 1, dtype=np.int64)
+    if n:
+        np.cumsum([len(e) for e in enc], out=off[1:])
+    blob = b"".join(enc)
+    ordr = None if order is None else np.ascontiguousarray(order, dtype=np.int64)
+    L = lib()
+    need = C.c_int64(0)
+    args = (_ptr(rec) if n else None, n, _ptr(ordr) if ordr is not None else None, blob, _ptr(off), int(n_threads))
+    rc = L.gvo_format_ranking_csv(*args, None, 0, C.byref(need))
+    if rc not in (0, STATUS_CAPACITY):
+        raise EngineError(rc, "gvo_format_ranking_csv: invalid arguments")
+    buf = C.create_string_buffer(max(1, need.value))
+    rc = L.gvo_format_ranking_csv(*args, buf, need.value, C.byref(need))
+    if rc != 0:
+        raise EngineError(rc, "gvo_format_ranking_csv failed")
+    return buf.raw[: need.value].decode()

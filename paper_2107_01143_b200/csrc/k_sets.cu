@@ -1181,7 +1181,9 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         U.key_lo = base;
         if (U.status == GVO_OK) {
           if (nr > 0 && (uint64_t)(U.key_hi - base) >= (uint64_t(1) << kKeyBits)) U.status = GVO_ERR_UNSUPPORTED;
-          if (acc > P.elem_cap) U.status = GVO_ERR_CAPACITY;
+          // oversized units are split into key ranges below when the split
+          // queue exists; only an unsplittable unit is capacity-bound
+          if (acc > P.elem_cap && !SS) U.status = GVO_ERR_CAPACITY;
         }
       }
       __syncthreads();
@@ -1231,6 +1233,19 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           range_a = 0;
           range_b = ((U.key_hi - U.key_lo) / U.R + 1) * U.R;
         }
+      }
+      if (!in_range && U.N > P.elem_cap) {  // split arena exhausted
+        if (threadIdx.x == 0) {
+          if (P.mode == 0) {
+            int64_t* row = P.counts + c * P.counts_stride;
+            atomicExch((unsigned long long*)&row[GVO_C_STATUS], (unsigned long long)GVO_ERR_CAPACITY);
+          } else {
+            atomicExch(P.status_out, GVO_ERR_CAPACITY);
+          }
+          if (SS) atomicAdd(&SS->pending, ~0ull);
+        }
+        __syncthreads();
+        continue;
       }
     } else {
       if (threadIdx.x == 0) {

@@ -11,6 +11,7 @@ ranks it with the device radix sort (key of perf.py:131).
 from __future__ import annotations
 
 from dataclasses import dataclass
+from collections.abc import Sequence
 from typing import Iterable, Mapping
 
 import numpy as np
@@ -129,18 +130,49 @@ def evaluate_sweep(family: KernelFamily, configs: Iterable[SweepConfig], machine
     return kept, kernels, res, order
 
 
+class SweepRows(Sequence):
+    """Ranked sweep rows (reference: list[SweepRow], perf.py:132).  Rows are
+    materialised on access from the device records; ``records`` / ``order``
+    / ``configs`` expose the batch for bulk consumers (the native ranking
+    CSV formatter, report.render_ranking_csv)."""
+
+    def __init__(self, kept, kernels, res, order):
+        self.configs = list(kept)
+        self._kernels = kernels
+        self._res = res
+        self.records = res.records
+        self.order = np.asarray(order, dtype=np.int64)
+
+    def __len__(self) -> int:
+        return len(self.order)
+
+    def _row(self, r: int) -> SweepRow:
+        i = int(self.order[r])
+        k, launch, flops = self._kernels[i]
+        return SweepRow(self.configs[i], _prediction(self._res, i, [f.name for f in k.fields], flops,
+                                                     _per_access(self._res, i, len(k.accesses))))
+
+    def __getitem__(self, idx):
+        if isinstance(idx, slice):
+            return [self._row(r) for r in range(*idx.indices(len(self)))]
+        r = int(idx)
+        if r < 0:
+            r += len(self)
+        if not 0 <= r < len(self):
+            raise IndexError("sweep row index out of range")
+        return self._row(r)
+
+    def __eq__(self, other):
+        return list(self) == list(other)
+
+
 def rank_sweep(family: KernelFamily, configs: Iterable[SweepConfig], machine: MachineDescriptor,
                fit_params: Mapping[str, GompertzParams] | None = None, *, block_samples: int = 5,
                wave_samples: int = 2, override_blocks_per_wave: int | None = None,
-               skip_invalid: bool = False) -> list[SweepRow]:
+               skip_invalid: bool = False) -> SweepRows:
     """Evaluate every configuration and order by descending predicted
     throughput, ties by (block_dim, folding) then input order (perf.py:98-132)."""
     kept, kernels, res, order = evaluate_sweep(
         family, configs, machine, fit_params, block_samples=block_samples, wave_samples=wave_samples,
         override_blocks_per_wave=override_blocks_per_wave, skip_invalid=skip_invalid)
-    rows = []
-    for i in order:
-        k, launch, flops = kernels[i]
-        rows.append(SweepRow(kept[i], _prediction(res, i, [f.name for f in k.fields], flops,
-                                                  _per_access(res, i, len(k.accesses)))))
-    return rows
+    return SweepRows(kept, kernels, res, order)
