@@ -93,7 +93,7 @@ struct gvo_ctx {
   // key-range splitting state: header + queue + descriptor arena
   DBuf<uint8_t> split_mem;
   SplitState* split = nullptr;
-  int64_t split_qcap = 1 << 22, split_arena = 256ll << 20;
+  int64_t split_qcap = 1 << 22, split_arena = 1024ll << 20;
   int64_t sm_cap = 0;  // GVO_SMEM_ELEMS test hook
   DBuf<uint8_t> rank_scratch;
   // host-variant staging

@@ -122,8 +122,54 @@ struct RunSink {
   int64_t* key_hi;
 };
 
+__device__ inline void emit_normalized(const RunSink& S, const Lat& L, int tag, const Granule& G);
+
+// Normalise, then split off the dimensions that interleave with faster
+// ones (a stride not beyond the reach of the kept faster dimensions, e.g. a
+// translate pair 192 B apart on a 120 B-stride row): the sub-lattices over
+// the remaining dimensions are monotone, so key ranges can bisect them
+// instead of scanning.  Splitting is bounded (<= 64 sub-lattices); beyond
+// that the lattice is emitted as one non-monotone run.
 __device__ inline void emit_lattice(const RunSink& S, Lat L, int tag, const Granule& G) {
   normalize(L, G.g);
+  int split[kMaxDims];
+  int ns = 0;
+  int64_t combos = 1;
+  {
+    unsigned __int128 reach = (unsigned __int128)L.span;
+    for (int d = 0; d < L.nd; ++d) {
+      if (d > 0 && (unsigned __int128)L.st[d] <= reach) {
+        split[ns++] = d;
+        combos *= L.ex[d];
+      } else {
+        reach += (unsigned __int128)L.st[d] * (uint64_t)(L.ex[d] - 1);
+      }
+    }
+  }
+  if (ns == 0 || combos > 64) { emit_normalized(S, L, tag, G); return; }
+  Lat K;
+  K.span = L.span;
+  K.nd = 0;
+  for (int d = 0, q = 0; d < L.nd; ++d) {
+    if (q < ns && split[q] == d) { ++q; continue; }
+    K.st[K.nd] = L.st[d];
+    K.ex[K.nd] = L.ex[d];
+    ++K.nd;
+  }
+  for (int64_t m = 0; m < combos; ++m) {
+    int64_t r = m;
+    uint64_t b = (uint64_t)L.base;
+    for (int q = 0; q < ns; ++q) {
+      const int d = split[q];
+      b += L.st[d] * (uint64_t)(r % L.ex[d]);
+      r /= L.ex[d];
+    }
+    K.base = (int64_t)b;
+    emit_normalized(S, K, tag, G);
+  }
+}
+
+__device__ inline void emit_normalized(const RunSink& S, const Lat& L, int tag, const Granule& G) {
   int64_t count = 1;
   uint64_t ext_span = L.span;
   for (int d = 0; d < L.nd; ++d) {
@@ -531,6 +577,98 @@ __device__ void sweep(const uint64_t* e, int64_t n, UnitSh& U, int64_t* wmax /* 
       int64_t v = 0;
       for (int k = 0; k < kNW; ++k) v += wmax[threadIdx.x * kNW + k];
       U.sub_val[s0 + threadIdx.x] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ bitmap tier
+// Exact set measures of one key range [a, b) by bitmaps: bit (t, x) is set
+// iff granule a + x lies in an interval of tag t.  Every in-range element of
+// the unit's runs sets its clipped bits (single-word intervals by one
+// shared-memory atomicOr, longer ones word by word), then each requested
+// measure is the popcount of the OR of its tags' words, at granule or at
+// line resolution (groups of r bits, r | 32, a aligned to r).
+__device__ __forceinline__ void bm_set(uint32_t* bm, int64_t x, int64_t y) {
+  const int64_t w0 = x >> 5, w1 = y >> 5;
+  const uint32_t m0 = ~0u << (x & 31), m1 = ~0u >> (31 - (y & 31));
+  if (w0 == w1) { atomicOr(bm + w0, m0 & m1); return; }
+  atomicOr(bm + w0, m0);
+  for (int64_t w = w0 + 1; w < w1; ++w) bm[w] = ~0u;  // idempotent: races with atomicOr are benign
+  atomicOr(bm + w1, m1);
+}
+
+__device__ __forceinline__ uint32_t bm_lines(uint32_t v, int r) {
+  // one bit per group of r bits that has any bit set (bit at the group's low end)
+  uint32_t low = 0;
+  for (int k = 0; k < 32; k += r) low |= 1u << k;
+  uint32_t o = v;
+  for (int k = 1; k < r; k <<= 1) o |= o >> k;  // OR-fold within groups (r a power of two)
+  return o & low;
+}
+
+__device__ void bitmap_range(uint32_t* bm, const Run* druns, const int64_t* rcnt, const int64_t* rka, int nr,
+                             int64_t N, int64_t a, int64_t b, int64_t kbase, int n_tags, const Granule& Gr,
+                             const TplView& T, int abase, const int64_t* fbase, const int32_t bd[3],
+                             const int64_t gd[3], int64_t tpb, UnitSh& U, int64_t* wmax) {
+  const int64_t wp = (b - a + 31) >> 5;
+  for (int64_t i = threadIdx.x; i < (int64_t)n_tags * wp; i += kNT) bm[i] = 0u;
+  __syncthreads();
+  // monotone runs: elements rka[r] .. rka[r] + count, contiguous per thread
+  {
+    const int64_t per = (N + kNT - 1) / kNT;
+    const int64_t e0 = min(N, (int64_t)threadIdx.x * per), e1 = min(N, e0 + per);
+    int ri = 0;
+    if (e0 < e1) {
+      int lo = 0, hi = nr - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (rcnt[mid] <= e0) lo = mid; else hi = mid - 1;
+      }
+      ri = lo;
+    }
+    for (int64_t i = e0; i < e1; ++i) {
+      while (rcnt[ri + 1] <= i) ++ri;
+      if (rka[ri] < 0) continue;
+      const Run& rr = druns[ri];
+      int64_t lo, hi;
+      run_interval(rr, rka[ri] + (i - rcnt[ri]), Gr, T, abase, fbase, bd, gd, tpb, &lo, &hi);
+      lo = max(lo - kbase, a);
+      hi = min(hi - kbase, b - 1);
+      if (lo <= hi) bm_set(bm + (int64_t)rr.tag * wp, lo - a, hi - a);
+    }
+  }
+  // non-monotone runs: every element, clipped
+  for (int r = 0; r < nr; ++r) {
+    if (rka[r] >= 0) continue;
+    const Run& rr = druns[r];
+    for (int64_t k = threadIdx.x; k < rr.count; k += kNT) {
+      int64_t lo, hi;
+      run_interval(rr, k, Gr, T, abase, fbase, bd, gd, tpb, &lo, &hi);
+      lo = max(lo - kbase, a);
+      hi = min(hi - kbase, b - 1);
+      if (lo <= hi) bm_set(bm + (int64_t)rr.tag * wp, lo - a, hi - a);
+    }
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q = 0; q < U.n_sub; ++q) {
+    const uint32_t mask = U.sub_mask[q];
+    const int r = (int)U.sub_r[q];
+    int64_t c = 0;
+    for (int64_t i = threadIdx.x; i < wp; i += kNT) {
+      uint32_t v = 0;
+      for (int t = 0; t < n_tags; ++t)
+        if ((mask >> t) & 1u) v |= bm[(int64_t)t * wp + i];
+      c += __popc(r == 1 ? v : bm_lines(v, r));
+    }
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) wmax[w] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t t = 0;
+      for (int k = 0; k < kNW; ++k) t += wmax[k];
+      U.sub_val[q] = t;
     }
     __syncthreads();
   }
@@ -1282,8 +1420,17 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       int64_t* rcnt = nr <= kSmemRuns ? roff_sh : roff_gl;
       int64_t* rka = nr <= kSmemRuns ? rka_sh : rka_gl;
       __shared__ int64_t s_N;
-      __shared__ int s_split;
+      __shared__ int s_split, s_bm;
       int64_t a = range_a, b = range_b;
+      // tags in use and whether every rescale divides a 32-bit word
+      int n_tags = 0;
+      bool bm_r_ok = true;
+      for (int q = 0; q < U.n_sub; ++q) {
+        const uint32_t m = U.sub_mask[q];
+        if (m) n_tags = max(n_tags, 32 - __clz((int)m));
+        bm_r_ok = bm_r_ok && U.sub_r[q] >= 1 && U.sub_r[q] <= 32 && (32 % U.sub_r[q]) == 0;
+      }
+      const int64_t bm_words = sm_elems * 4;  // ebuf holds 2*sm_elems 8-byte elements
       for (;;) {
         // count in-range elements per run (monotone runs: bisection)
         for (int r = threadIdx.x; r < nr; r += kNT) {
@@ -1326,7 +1473,14 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           rcnt[nr] = acc;
           s_N = acc;
           s_split = 0;
-          if (acc > sm_elems && b - a > R) {
+          // bitmap tier: one bit per granule and tag over [a, b) in the
+          // element buffer, when the range is narrow enough and dense enough
+          // that setting bits beats emitting + radix sorting intervals
+          const int64_t wp = (b - a + 31) >> 5;
+          const bool bm_fit = bm_r_ok && (int64_t)n_tags * wp <= bm_words;
+          const bool bm_cheaper = acc * 96 > (int64_t)n_tags * wp * 2 + wp * 3 * (int64_t)U.n_sub;
+          s_bm = bm_fit && (acc > sm_elems || bm_cheaper) ? 1 : 0;
+          if (!s_bm && acc > sm_elems && b - a > R) {
             const int64_t mid = a + ((b - a) / (2 * R)) * R;
             if (mid > a && mid < b) {
               atomicAdd(&hdr->outstanding, 1);
@@ -1358,7 +1512,11 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         if (!s_split) break;
       }
       const int64_t N = s_N;
-      if (N > P.elem_cap) {
+      if (s_bm) {
+        bitmap_range(reinterpret_cast<uint32_t*>(ebuf), druns, rcnt, rka, nr, N, a, b, kbase, n_tags, Gr, P.T, abase,
+                     fbase, bd, gd, tpb, U, wmax);
+        if (threadIdx.x < U.n_sub) atomicAdd(&hdr->acc[threadIdx.x], (unsigned long long)U.sub_val[threadIdx.x]);
+      } else if (N > P.elem_cap) {
         if (threadIdx.x == 0) atomicExch(&hdr->status, GVO_ERR_CAPACITY);
       } else {
         uint64_t* A0 = N <= sm_elems ? ebuf : gbuf;

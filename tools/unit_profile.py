@@ -1,4 +1,5 @@
-"""Per-unit cost profile of the interval-union engine on the C2 workload (GPU)."""
+"""Per-unit cost profile of the interval-union engine on a bench workload (GPU).
+usage: python tools/unit_profile.py [C2|C3|C4]"""
 import sys, json
 from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
@@ -9,8 +10,10 @@ from paper_2107_01143_b200 import _native
 
 ctx = _native.context()
 L = _native.lib()
-batch, kept = bench.build_shard(0)
-cfgs = batch.config_array()
+wl = sys.argv[1] if len(sys.argv) > 1 else "C2"
+sp, _, _ = bench.build_shard(wl, 0, 1)
+cfgs = sp.config_array(ctx)
+kept = [type("K", (), {"key": sp.key(i)})() for i in range(len(sp))]
 L.gvo_debug_units(ctx.h, 1, None, 0, None)
 for _ in range(2):
     out = ctx.eval_configs_host(cfgs, 5, 2, 0)
