@@ -15,7 +15,7 @@ from pathlib import Path
 import numpy as np
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libgvo_b200.so"
+LIB_PATH = _HERE / ("libgvo_b200_prof.so" if os.environ.get("GVO_LIB_VARIANT") == "prof" else "libgvo_b200.so")
 
 GVO_MAX_FIELDS = 16
 GVO_MAX_ACCESSES = 1024

@@ -17,12 +17,16 @@ from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
-OBJ = HERE / "build" / "obj"
-LIB = HERE / "libgvo_b200.so"
+# GVO_BUILD_VARIANT=prof: same sources with the set kernel's per-CTA phase
+# counters compiled in (tools/unit_profile.py), as a separate library
+VARIANT = os.environ.get("GVO_BUILD_VARIANT", "")
+OBJ = HERE / "build" / ("obj_" + VARIANT if VARIANT else "obj")
+LIB = HERE / ("libgvo_b200_" + VARIANT + ".so" if VARIANT else "libgvo_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
-                "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr"]
+                "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr"] + (
+                    ["-DGVO_PHASE_STATS=1"] if VARIANT == "prof" else [])
 
 
 def _headers():

@@ -86,15 +86,16 @@ struct gvo_ctx {
   DBuf<int64_t> ctabs;
   DBuf<Geo> geos;
   DBuf<uint8_t> slab;
-  int64_t run_cap = 4096, elem_cap = 1 << 19, slab_bytes = 0;
+  int64_t run_cap = 16384, elem_cap = 1 << 19, slab_bytes = 0;
   int n_ctas = 0;
   DBuf<int> status;
   DBuf<unsigned long long> work;
   // key-range splitting state: header + queue + descriptor arena
   DBuf<uint8_t> split_mem;
   SplitState* split = nullptr;
-  int64_t split_qcap = 1 << 22, split_arena = 1024ll << 20;
+  int64_t split_qcap = 1 << 22, split_arena = 4096ll << 20;
   int64_t sm_cap = 0;  // GVO_SMEM_ELEMS test hook
+  int32_t seg_off = 0; // GVO_SEG=0 disables the segment cover (A/B hook)
   DBuf<uint8_t> rank_scratch;
   // host-variant staging
   DBuf<gvo_config> s_cfgs;
@@ -163,6 +164,7 @@ int gvo_open(int device, gvo_ctx** out) {
   if (const char* e = getenv("GVO_RUN_CAP")) ctx->run_cap = atoll(e);
   if (const char* e = getenv("GVO_BATCH")) ctx->batch = atoll(e);
   if (const char* e = getenv("GVO_SMEM_ELEMS")) ctx->sm_cap = atoll(e);
+  if (const char* e = getenv("GVO_SEG")) ctx->seg_off = atoi(e) == 0;
   ctx->n_ctas = kSetsCtasPerSm * ctx->n_sm;
   *out = ctx;
   return GVO_OK;
@@ -404,13 +406,14 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     L.work = ctx->work.p;
     L.split = ctx->split;
     L.sm_cap = ctx->sm_cap;
+    L.seg_off = ctx->seg_off;
     if (fuse) {
       L.warp = WA;
       L.n_warp_items = WA.n_items;
     }
     if (ctx->unit_debug) {
-      if (!ctx->unit_stats.ensure((size_t)L.n_items * 10 + 10 + 4096 * 10)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
-      CK(cudaMemsetAsync(ctx->unit_stats.p, 0, ((size_t)L.n_items * 10 + 10 + 4096 * 10) * 8, st));
+      if (!ctx->unit_stats.ensure((size_t)L.n_items * 10 + 10 + 4096 * 10 + 1024 * 16)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
+      CK(cudaMemsetAsync(ctx->unit_stats.p, 0, ((size_t)L.n_items * 10 + 10 + 4096 * 10 + 1024 * 16) * 8, st));
       L.unit_stats = ctx->unit_stats.p;
       ctx->unit_items = L.n_items;
     }
@@ -544,6 +547,7 @@ int gvo_group_footprint(gvo_ctx* ctx, int32_t tpl, const int32_t block[3], const
   L.work = ctx->work.p;
   L.split = ctx->split;
     L.sm_cap = ctx->sm_cap;
+    L.seg_off = ctx->seg_off;
   launch_sets(L, st);
   launch_warp(ctx->view, ctx->d_machines.p, ctx->s_cfgs.p, ctx->geos.p, ctx->coefs.p, (int64_t)blocks.size(), 0, granularity, 1, 1, 1,
               ctx->s_i64c.p, nullptr, 0, F, nullptr, 0, ctx->s_ull.p, ctx->max_acc, ctx->n_sm, st);
@@ -607,6 +611,7 @@ int gvo_group_sets(gvo_ctx* ctx, int32_t tpl, const int32_t block[3], const int6
   L.work = ctx->work.p;
   L.split = ctx->split;
     L.sm_cap = ctx->sm_cap;
+    L.seg_off = ctx->seg_off;
   launch_sets(L, st);
   CK(cudaGetLastError());
   int status = 0;
@@ -713,7 +718,7 @@ int gvo_debug_units(gvo_ctx* ctx, int enable, int64_t* h_out, int64_t cap, int64
   if (n_items) *n_items = ctx->unit_items;
   if (h_out && ctx->unit_items) {
     CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(h_out, ctx->unit_stats.p, std::min<int64_t>(cap, ctx->unit_items * 10 + 10 + 4096 * 10) * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(h_out, ctx->unit_stats.p, std::min<int64_t>(cap, ctx->unit_items * 10 + 10 + 4096 * 10 + 1024 * 16) * 8, cudaMemcpyDeviceToHost));
   }
   return GVO_OK;
 }

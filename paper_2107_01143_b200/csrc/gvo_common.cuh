@@ -235,6 +235,8 @@ struct SplitHdr {
   unsigned long long acc[kMaxSubC];
   int32_t outstanding;
   int32_t status;
+  uint32_t tag_mask;  // tags present in the runs (bitmap tier: compact tags)
+  int32_t pad_;
 };
 struct RangeItem {
   int64_t desc;  // byte offset of the SplitHdr in the arena

@@ -54,6 +54,7 @@ struct SetsLaunch {
   int64_t n_warp_items = 0;
   SplitState* split = nullptr;
   int64_t sm_cap = 0;
+  int32_t seg_off = 0;
 };
 int64_t sets_ebuf_bytes();
 void launch_sets(const SetsLaunch& L, cudaStream_t st);

@@ -25,6 +25,14 @@
 
 namespace gvo {
 
+// per-CTA phase accounting for tools/unit_profile.py (build with
+// GVO_PHASE_STATS=1); compiled out of the product kernel
+#if defined(GVO_PHASE_STATS) && GVO_PHASE_STATS
+#define GVO_PH(...) __VA_ARGS__
+#else
+#define GVO_PH(...)
+#endif
+
 constexpr int kNT = 512;           // threads per CTA
 constexpr int kNW = kNT / 32;
 constexpr int kMaxSrc = 64;        // sources per unit
@@ -45,6 +53,7 @@ struct UnitSh {
   int64_t sub_r[kMaxSub];
   int sub_sh[kMaxSub];      // log2(sub_r) when a power of two, else -1
   int64_t sub_val[kMaxSub];
+  uint32_t sub_cm[kMaxSub];  // bitmap tier: subset masks over the compact tags
   int64_t g, R;
   int status;
   int n_runs;
@@ -215,7 +224,7 @@ __device__ inline void emit_normalized(const RunSink& S, const Lat& L, int tag, 
 // point starts or continues exactly one maximal ray along that stride), so
 // all rays of a dimension are judged in parallel against the points not yet
 // covered by larger-stride rays; the same greedy as cover_and_emit.
-__device__ void cover_warp(const RunSink& S, const Lat& L0, const int64_t* P, int n, int tag,
+__device__ __noinline__ void cover_warp(const RunSink& S, const Lat& L0, const int64_t* P, int n, int tag,
                            const Granule& G) {
   const int lane = threadIdx.x & 31;
   uint64_t req = n >= 64 ? ~0ull : ((1ull << n) - 1);
@@ -316,6 +325,315 @@ __device__ void cover_warp(const RunSink& S, const Lat& L0, const int64_t* P, in
   }
 }
 
+// ------------------------------------------------------------------ segments
+// Translates of a point lattice whose residues modulo the fastest stride
+// tile whole cells (zyxf layouts: the Q components of a cell are adjacent
+// words, and every pull load is the same lattice shifted by a neighbour
+// cell).  cover_warp finds no rays or clusters there and each translate
+// stays a lattice of points.  Instead: write every translate as
+// residue + lattice-coordinate offset, so translate p covers the box
+// B_p = prod_d [k_pd, k_pd + ex_d) with its residue.  The boundaries of all
+// B_p cut coordinate space into segment boxes on which the set of present
+// translates is fixed; their residues cluster into spans, and where every
+// translate is present the cluster covers a whole cell, folds into the span
+// and rows collapse into intervals.  Exact: the segment boxes partition the
+// union of the B_p (any decomposition of the offsets is valid).
+constexpr int kSegDims = 4;
+constexpr int kSegBp = 66;          // breakpoints per dimension (<= 65 used: 64 segments)
+constexpr int kSegMaxBoxes = 4096;
+constexpr int kSegScratch = 2688;   // bytes of per-warp scratch
+constexpr int64_t kSegRunWeight = 48;  // element-equivalents of one extra run
+struct SegScratch {
+  int32_t kv[kSegDims][64];  // offsets per dimension, by translate
+  int32_t bp[kSegDims][kSegBp];
+  int32_t rs[64];            // residues, sorted
+  int32_t tmp[64];
+  int32_t nb[kSegDims];
+  uint8_t ord[64];           // sorted position -> translate
+};
+static_assert(sizeof(SegScratch) <= kSegScratch, "segment scratch");
+
+__device__ __forceinline__ int64_t floordiv128(__int128 a, __int128 b, __int128* rem) {
+  __int128 q = a / b;
+  __int128 r = a - q * b;
+  if (r != 0 && ((r < 0) != (b < 0))) { q -= 1; r += b; }
+  *rem = r;
+  return (int64_t)q;
+}
+
+// Returns false (nothing emitted) when the class is not of that shape or
+// the segment plan is not cheaper than cover_warp's.
+__device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, const int64_t* P, int n, int tag,
+                               const Granule& G, SegScratch* sc) {
+  const int lane = threadIdx.x & 31;
+  const int nd = L0.nd;
+  if (nd < 1 || nd > kSegDims || n < 2 || n > 64) return false;
+  const uint64_t s0 = L0.st[0];
+  if (s0 >= (uint64_t(1) << 30) || L0.span >= s0) return false;
+  for (int d = 0; d < nd; ++d)
+    if (L0.ex[d] >= (int64_t(1) << 29) || L0.st[d] >= (uint64_t(1) << 62)) return false;
+  const int64_t tol = (int64_t)L0.span + G.g;
+  if ((int64_t)n * tol < (int64_t)s0) return false;  // n residues cannot tile a cell
+  // 1. offsets: round to nearest along the outer dims, floor along dim 0
+  bool ok = true;
+  for (int i = lane; i < n; i += 32) {
+    const __int128 off0 = (__int128)P[i] - (__int128)L0.base;
+    if (off0 > -(__int128(1) << 60) && off0 < (__int128(1) << 60)) {
+      int64_t off = (int64_t)off0;  // strides < 2^62: no overflow below
+      for (int d = nd - 1; d >= 1; --d) {
+        const int64_t s = (int64_t)L0.st[d];
+        const int64_t k = floordiv(off + s / 2, s);
+        off -= k * s;
+        if (k < -(int64_t(1) << 28) || k > (int64_t(1) << 28)) ok = false;
+        sc->kv[d][i] = (int32_t)k;
+      }
+      const int64_t k0 = floordiv(off, (int64_t)s0);
+      if (k0 < -(int64_t(1) << 28) || k0 > (int64_t(1) << 28)) ok = false;
+      sc->kv[0][i] = (int32_t)k0;
+      sc->tmp[i] = (int32_t)(off - k0 * (int64_t)s0);  // [0, s0)
+    } else {
+      __int128 off = off0, rem;
+      for (int d = nd - 1; d >= 1; --d) {
+        const __int128 s = (__int128)L0.st[d];
+        const int64_t k = floordiv128(off + s / 2, s, &rem);
+        off -= (__int128)k * s;
+        if (k < -(int64_t(1) << 28) || k > (int64_t(1) << 28)) ok = false;
+        sc->kv[d][i] = (int32_t)k;
+      }
+      const int64_t k0 = floordiv128(off, (__int128)s0, &rem);
+      if (k0 < -(int64_t(1) << 28) || k0 > (int64_t(1) << 28)) ok = false;
+      sc->kv[0][i] = (int32_t)k0;
+      sc->tmp[i] = (int32_t)rem;  // [0, s0)
+    }
+  }
+  if (!__all_sync(0xffffffffu, ok)) return false;
+  __syncwarp();
+  // 2. residues sorted (rank sort, ties by index); ord maps back
+  {
+    int32_t v[2];
+    int rk[2];
+    for (int t = 0; t < 2; ++t) {
+      const int i = lane + 32 * t;
+      rk[t] = -1;
+      if (i < n) {
+        v[t] = sc->tmp[i];
+        int r = 0;
+        for (int j = 0; j < n; ++j) {
+          const int32_t u = sc->tmp[j];
+          r += (u < v[t]) || (u == v[t] && j < i);
+        }
+        rk[t] = r;
+      }
+    }
+    __syncwarp();
+    for (int t = 0; t < 2; ++t)
+      if (rk[t] >= 0) { sc->rs[rk[t]] = v[t]; sc->ord[rk[t]] = (uint8_t)(lane + 32 * t); }
+    __syncwarp();
+  }
+  // residues must tile the cell: consecutive gaps (and the wrap) <= span + g
+  bool cont = true;
+  for (int r = lane; r < n; r += 32) {
+    const int64_t nx = r + 1 < n ? (int64_t)sc->rs[r + 1] : (int64_t)sc->rs[0] + (int64_t)s0;
+    if (nx - (int64_t)sc->rs[r] > tol) cont = false;
+  }
+  if (!__all_sync(0xffffffffu, cont)) return false;
+  // 3. breakpoints per dimension: distinct offsets D, merged with D + ex
+  int64_t nbox = 1;
+  for (int d = 0; d < nd; ++d) {
+    const int32_t ex = (int32_t)L0.ex[d];
+    int32_t v[2];
+    int rk[2];
+    for (int t = 0; t < 2; ++t) {
+      const int i = lane + 32 * t;
+      rk[t] = -1;
+      if (i < n) {
+        v[t] = sc->kv[d][i];
+        int r = 0;
+        bool first = true;
+        for (int j = 0; j < n; ++j) {
+          const int32_t u = sc->kv[d][j];
+          if (u == v[t] && j < i) first = false;
+          r += u < v[t];
+        }
+        // rank among distinct values = #distinct values below v
+        if (first) rk[t] = r;
+      }
+    }
+    // compact: distinct rank = number of distinct values below -> count of
+    // first occurrences below (computed by ballot over sorted ranks)
+    __syncwarp();
+    // tmp[r] = value for first occurrences at their (non-distinct) rank
+    for (int j = lane; j < n; j += 32) sc->tmp[j] = INT32_MIN;
+    __syncwarp();
+    for (int t = 0; t < 2; ++t) if (rk[t] >= 0) sc->tmp[rk[t]] = v[t];
+    __syncwarp();
+    // distinct sorted values: the non-sentinel entries of tmp in order
+    int m = 0;
+    {
+      const int32_t a0 = lane < n ? sc->tmp[lane] : INT32_MIN;
+      const int32_t a1 = lane + 32 < n ? sc->tmp[lane + 32] : INT32_MIN;
+      const unsigned b0 = __ballot_sync(0xffffffffu, a0 != INT32_MIN);
+      const unsigned b1 = __ballot_sync(0xffffffffu, a1 != INT32_MIN);
+      const int p0 = __popc(b0 & ((1u << lane) - 1u));
+      const int p1 = __popc(b0) + __popc(b1 & ((1u << lane) - 1u));
+      m = __popc(b0) + __popc(b1);
+      __syncwarp();
+      if (a0 != INT32_MIN) sc->tmp[p0] = a0;  // p0 <= lane: safe after the reads above
+      __syncwarp();
+      if (a1 != INT32_MIN) sc->tmp[p1] = a1;
+      __syncwarp();
+    }
+    // merge D (tmp[0..m), sorted distinct) with D + ex, common values once
+    auto lbD = [&](int32_t x) {  // #D elements < x
+      int lo = 0, hi = m;
+      while (lo < hi) { const int mid = (lo + hi) >> 1; if (sc->tmp[mid] < x) lo = mid + 1; else hi = mid; }
+      return lo;
+    };
+    uint64_t both = 0;  // D elements y with y - ex in D (y in D and in D + ex)
+    for (int t = 0; t < 2; ++t) {
+      const int i = lane + 32 * t;
+      bool f = false;
+      if (i < m) { const int32_t y = sc->tmp[i] - ex; const int j = lbD(y); f = j < m && sc->tmp[j] == y; }
+      const unsigned bb = __ballot_sync(0xffffffffu, f);
+      both |= (uint64_t)bb << (32 * t);
+    }
+    const int nmerged = 2 * m - __popcll(both);
+    if (nmerged > kSegBp - 1) return false;
+    for (int t = 0; t < 2; ++t) {
+      const int i = lane + 32 * t;
+      if (i >= m) continue;
+      const int32_t x = sc->tmp[i];
+      const uint64_t below_i = i ? (~0ull >> (64 - i)) : 0ull;
+      sc->bp[d][i + lbD(x - ex) - __popcll(both & below_i)] = x;
+      const int32_t y = x + ex;
+      const int j = lbD(y);
+      if (!(j < m && sc->tmp[j] == y)) {
+        const uint64_t below_j = j ? (j >= 64 ? ~0ull : (~0ull >> (64 - j))) : 0ull;
+        sc->bp[d][j + i - __popcll(both & below_j)] = y;
+      }
+    }
+    if (lane == 0) sc->nb[d] = nmerged;
+    nbox *= nmerged - 1;
+    if (nbox > kSegMaxBoxes) return false;
+    __syncwarp();
+  }
+  // 4. per-dimension segment masks over sorted positions (lane holds
+  // segments lane and lane + 32)
+  uint64_t segm[kSegDims][2];
+#pragma unroll
+  for (int d = 0; d < kSegDims; ++d) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      segm[d][h] = 0;
+      const int sg = lane + 32 * h;
+      if (d < nd && sg < sc->nb[d] - 1) {
+        const int32_t lo = sc->bp[d][sg], hi = sc->bp[d][sg + 1];
+        const int32_t ex = (int32_t)L0.ex[d];
+        for (int r = 0; r < n; ++r) {
+          const int32_t k = sc->kv[d][sc->ord[r]];
+          if (k <= lo && hi <= k + ex) segm[d][h] |= 1ull << r;
+        }
+      }
+    }
+  }
+  // 5. plan: elements and runs of the segment cover vs. cover_warp's clusters
+  double vol0 = 1.0;
+  for (int d = 0; d < nd; ++d) vol0 *= (double)L0.ex[d];
+  double seg_el = 0.0;
+  int64_t seg_runs = 0;
+  for (int64_t b0 = 0; b0 < nbox; b0 += 32) {
+    const int64_t b = b0 + lane;
+    int sd[kSegDims];
+    {
+      int64_t r = b < nbox ? b : 0;
+#pragma unroll
+      for (int d = 0; d < kSegDims; ++d) {
+        if (d < nd) { const int ns = sc->nb[d] - 1; sd[d] = (int)(r % ns); r /= ns; } else sd[d] = 0;
+      }
+    }
+    uint64_t M = ~0ull;
+#pragma unroll
+    for (int d = 0; d < kSegDims; ++d) {
+      const uint64_t v0 = __shfl_sync(0xffffffffu, segm[d][0], sd[d] & 31);
+      const uint64_t v1 = __shfl_sync(0xffffffffu, segm[d][1], sd[d] & 31);
+      if (d < nd) M &= sd[d] >= 32 ? v1 : v0;
+    }
+    if (b >= nbox || !M) continue;
+    double vol = 1.0;
+    for (int d = 0; d < nd; ++d) vol *= (double)(sc->bp[d][sd[d] + 1] - sc->bp[d][sd[d]]);
+    const double len0 = (double)(sc->bp[0][sd[0] + 1] - sc->bp[0][sd[0]]);
+    uint64_t mm = M;
+    while (mm) {
+      const int r0 = __ffsll((long long)mm) - 1;
+      int r1 = r0;
+      mm &= mm - 1;
+      while (mm) {
+        const int q = __ffsll((long long)mm) - 1;
+        if ((int64_t)sc->rs[q] - (int64_t)sc->rs[r1] > tol) break;
+        r1 = q;
+        mm &= mm - 1;
+      }
+      const bool fold = (int64_t)s0 <= (int64_t)L0.span + (sc->rs[r1] - sc->rs[r0]) + G.g;
+      seg_el += fold ? vol / len0 : vol;
+      ++seg_runs;
+    }
+  }
+  int64_t n_cl = 0;  // cover_warp's clusters of consecutive translates
+  for (int i = lane; i < n; i += 32)
+    if (i == 0 || (unsigned __int128)(uint64_t)(P[i] - P[i - 1]) > (unsigned __int128)(uint64_t)tol) ++n_cl;
+  for (int o = 16; o; o >>= 1) {
+    seg_el += __shfl_xor_sync(0xffffffffu, seg_el, o);
+    seg_runs += __shfl_xor_sync(0xffffffffu, seg_runs, o);
+    n_cl += __shfl_xor_sync(0xffffffffu, n_cl, o);
+  }
+  if (seg_el + (double)(kSegRunWeight * seg_runs) >= (double)n_cl * vol0 + (double)(kSegRunWeight * n_cl)) return false;
+  // 6. emit
+  for (int64_t b0 = 0; b0 < nbox; b0 += 32) {
+    const int64_t b = b0 + lane;
+    int sd[kSegDims];
+    {
+      int64_t r = b < nbox ? b : 0;
+#pragma unroll
+      for (int d = 0; d < kSegDims; ++d) {
+        if (d < nd) { const int ns = sc->nb[d] - 1; sd[d] = (int)(r % ns); r /= ns; } else sd[d] = 0;
+      }
+    }
+    uint64_t M = ~0ull;
+#pragma unroll
+    for (int d = 0; d < kSegDims; ++d) {
+      const uint64_t v0 = __shfl_sync(0xffffffffu, segm[d][0], sd[d] & 31);
+      const uint64_t v1 = __shfl_sync(0xffffffffu, segm[d][1], sd[d] & 31);
+      if (d < nd) M &= sd[d] >= 32 ? v1 : v0;
+    }
+    if (b >= nbox || !M) continue;
+    Lat L;
+    L.nd = nd;
+    uint64_t base = (uint64_t)L0.base;
+    for (int d = 0; d < nd; ++d) {
+      L.st[d] = L0.st[d];
+      L.ex[d] = (int64_t)(sc->bp[d][sd[d] + 1] - sc->bp[d][sd[d]]);
+      base += L0.st[d] * (uint64_t)(int64_t)sc->bp[d][sd[d]];
+    }
+    uint64_t mm = M;
+    while (mm) {
+      const int r0 = __ffsll((long long)mm) - 1;
+      int r1 = r0;
+      mm &= mm - 1;
+      while (mm) {
+        const int q = __ffsll((long long)mm) - 1;
+        if ((int64_t)sc->rs[q] - (int64_t)sc->rs[r1] > tol) break;
+        r1 = q;
+        mm &= mm - 1;
+      }
+      Lat C = L;
+      C.base = (int64_t)(base + (uint64_t)(int64_t)sc->rs[r0]);
+      C.span = L0.span + (uint64_t)(sc->rs[r1] - sc->rs[r0]);
+      emit_lattice(S, C, tag, G);
+    }
+  }
+  return true;
+}
+
 // lattice of one coefficient vector over one block box, translation 0
 __device__ inline Lat box_lattice(const int64_t* c, const int32_t bd[3], const Box& b, const Granule& G) {
   Lat L;
@@ -398,20 +716,38 @@ __device__ __forceinline__ void run_interval(const Run& r, int64_t k, const Gran
 
 // first tuple k of a monotone run with (hi ? interval end : start) >= v
 __device__ inline int64_t mono_first(const Run& r, const Granule& Gr, int64_t kbase, int64_t v, bool hi) {
-  int64_t lo = 0, up = r.count;  // pieces == 1 for monotone runs
-  while (lo < up) {
-    const int64_t mid = (lo + up) >> 1;
-    const uint64_t b = run_base(r, mid);
-    const int64_t x = Gr.of((int64_t)(hi ? b + r.span : b)) - kbase;
-    if (x >= v) up = mid; else lo = mid + 1;
+  // f(k) = base + sum_d stride_d k_d increases with the tuple index (the
+  // monotone condition), so floor((f + span?)/g) - kbase >= v <=> f >= T:
+  // the digits of the first such tuple follow greedily from the slowest dim.
+  const __int128 T = ((__int128)v + (__int128)kbase) * (__int128)Gr.g - (hi ? (__int128)r.span : (__int128)0);
+  const __int128 R0 = T - (__int128)r.base;
+  if (R0 <= 0) return 0;
+  int64_t M[kMaxDims];  // reach of the dims faster than d
+  uint64_t acc = 0;
+  for (int d = 0; d < r.nd; ++d) { M[d] = (int64_t)acc; acc += (uint64_t)r.stride[d] * (uint64_t)(r.ext[d] - 1); }
+  if (R0 > (__int128)acc) return r.count;
+  int64_t R = (int64_t)R0;
+  int64_t mul = 1;
+  for (int d = 0; d < r.nd; ++d) mul *= r.ext[d];
+  int64_t idx = 0;
+  for (int d = r.nd - 1; d >= 0; --d) {
+    mul /= r.ext[d];
+    int64_t k = 0;
+    if (R > M[d]) {
+      const uint64_t st = (uint64_t)r.stride[d];
+      k = (int64_t)(((uint64_t)(R - M[d]) + st - 1) / st);
+      if (k > r.ext[d] - 1) k = r.ext[d] - 1;
+      R -= (int64_t)((uint64_t)k * st);
+    }
+    idx += k * mul;
   }
-  return lo;
+  return idx;
 }
 
 // ------------------------------------------------------------------ sort
 // CTA-wide stable LSD radix sort (8-bit digits) of packed 64-bit elements
 // on bits [bit0, bit0 + nbits).  a/b may live in shared or global memory.
-__device__ uint64_t* cta_sort(uint64_t* a, uint64_t* b, int64_t n, int bit0, int nbits,
+__device__ __noinline__ uint64_t* cta_sort(uint64_t* a, uint64_t* b, int64_t n, int bit0, int nbits,
                               uint32_t* hist /* kNW*256 */, uint32_t* tot /* 256 */) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t chunk = (((n + kNW - 1) / kNW) + 255) & ~int64_t(255);
@@ -499,7 +835,7 @@ __device__ uint64_t* cta_sort(uint64_t* a, uint64_t* b, int64_t n, int bit0, int
 // give each lane the running maximum R before its sub-chunk.  Pass 2: a
 // sequential walk adds max(0, hi - max(lo - 1, R)) per selected interval.
 constexpr int kSubGroup = 4;
-__device__ void sweep(const uint64_t* e, int64_t n, UnitSh& U, int64_t* wmax /* kMaxSub*kNW */) {
+__device__ __noinline__ void sweep(const uint64_t* e, int64_t n, UnitSh& U, int64_t* wmax /* kMaxSub*kNW */) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t chunk = (n + kNW - 1) / kNW;
   const int64_t beg = min(n, (int64_t)w * chunk), end = min(n, beg + chunk);
@@ -582,6 +918,27 @@ __device__ void sweep(const uint64_t* e, int64_t n, UnitSh& U, int64_t* wmax /* 
   }
 }
 
+// exclusive prefix sum of a[0..n) in place, total in a[n] (all threads)
+__device__ void cta_scan_excl(int64_t* a, int64_t n, int64_t* wtmp /* kNW */) {
+  const int64_t per = (n + kNT - 1) / kNT;
+  const int64_t b0 = min(n, (int64_t)threadIdx.x * per), b1 = min(n, b0 + per);
+  int64_t s = 0;
+  for (int64_t i = b0; i < b1; ++i) s += a[i];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t inc = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) wtmp[w] = inc;
+  __syncthreads();
+  int64_t run = inc - s;
+  for (int k = 0; k < w; ++k) run += wtmp[k];
+  for (int64_t i = b0; i < b1; ++i) { const int64_t v = a[i]; a[i] = run; run += v; }
+  if (threadIdx.x == kNT - 1) a[n] = run;
+  __syncthreads();
+}
+
 // ------------------------------------------------------------------ bitmap tier
 // Exact set measures of one key range [a, b) by bitmaps: bit (t, x) is set
 // iff granule a + x lies in an interval of tag t.  Every in-range element of
@@ -607,14 +964,56 @@ __device__ __forceinline__ uint32_t bm_lines(uint32_t v, int r) {
   return o & low;
 }
 
-__device__ void bitmap_range(uint32_t* bm, const Run* druns, const int64_t* rcnt, const int64_t* rka, int nr,
+// Bits of elements [k, k + cnt) of one monotone lattice run in the bitmap of
+// its tag (bit x = granule kb0 + x, x < w).  Dim 0 is stepped incrementally;
+// single-granule intervals landing in the same word are OR-ed in a register
+// and written with one atomicOr.  Kept out of line: few live values, no spills.
+__device__ __noinline__ void bm_lattice(uint32_t* bmt, const Run* rrp, int64_t k, int64_t cnt, int64_t kb0,
+                                        int64_t w, int64_t g, int shift) {
+  const Run& rr = *rrp;
+  const int nd = rr.nd;
+  const uint64_t st0 = nd ? (uint64_t)rr.stride[0] : 0;
+  const int64_t ex0 = nd ? rr.ext[0] : 1;
+  const uint64_t span = rr.span;
+  uint64_t bb = run_base(rr, k);
+  int64_t i0 = nd ? k % ex0 : 0;
+  uint32_t* cur_p = nullptr;
+  uint32_t cur_m = 0;
+  for (int64_t t = 0; t < cnt; ++t) {
+    int64_t lo, hi;
+    if (shift >= 0) { lo = ((int64_t)bb >> shift) - kb0; hi = ((int64_t)(bb + span) >> shift) - kb0; }
+    else { lo = floordiv((int64_t)bb, g) - kb0; hi = floordiv((int64_t)(bb + span), g) - kb0; }
+    lo = max(lo, (int64_t)0);
+    hi = min(hi, w - 1);
+    if (lo == hi) {
+      uint32_t* p = bmt + (lo >> 5);
+      const uint32_t bit = 1u << (lo & 31);
+      if (p == cur_p) cur_m |= bit;
+      else {
+        if (cur_p) atomicOr(cur_p, cur_m);
+        cur_p = p;
+        cur_m = bit;
+      }
+    } else if (lo < hi) {
+      bm_set(bmt, lo, hi);
+    }
+    if (++i0 < ex0) bb += st0;
+    else { i0 = 0; if (t + 1 < cnt) bb = run_base(rr, k + t + 1); }
+  }
+  if (cur_p) atomicOr(cur_p, cur_m);
+}
+
+__device__ __noinline__ void bitmap_range(uint32_t* bm, const Run* druns, const int64_t* rcnt, const int64_t* rka, int nr,
                              int64_t N, int64_t a, int64_t b, int64_t kbase, int n_tags, const Granule& Gr,
                              const TplView& T, int abase, const int64_t* fbase, const int32_t bd[3],
-                             const int64_t gd[3], int64_t tpb, UnitSh& U, int64_t* wmax) {
+                             const int64_t gd[3], int64_t tpb, UnitSh& U, int64_t* wmax, bool nonmono,
+                             uint32_t tag_mask) {
   const int64_t wp = (b - a + 31) >> 5;
   for (int64_t i = threadIdx.x; i < (int64_t)n_tags * wp; i += kNT) bm[i] = 0u;
   __syncthreads();
-  // monotone runs: elements rka[r] .. rka[r] + count, contiguous per thread
+  // monotone runs: elements rka[r] .. rka[r] + count, contiguous per thread.
+  // Dim 0 is stepped incrementally; single-granule intervals that land in
+  // the same bitmap word are OR-ed in a register before one atomicOr.
   {
     const int64_t per = (N + kNT - 1) / kNT;
     const int64_t e0 = min(N, (int64_t)threadIdx.x * per), e1 = min(N, e0 + per);
@@ -627,19 +1026,32 @@ __device__ void bitmap_range(uint32_t* bm, const Run* druns, const int64_t* rcnt
       }
       ri = lo;
     }
-    for (int64_t i = e0; i < e1; ++i) {
+    int64_t i = e0;
+    while (i < e1) {
       while (rcnt[ri + 1] <= i) ++ri;
-      if (rka[ri] < 0) continue;
+      const int64_t iend = min(e1, rcnt[ri + 1]);
+      if (rka[ri] < 0) { i = iend; continue; }
       const Run& rr = druns[ri];
-      int64_t lo, hi;
-      run_interval(rr, rka[ri] + (i - rcnt[ri]), Gr, T, abase, fbase, bd, gd, tpb, &lo, &hi);
-      lo = max(lo - kbase, a);
-      hi = min(hi - kbase, b - 1);
-      if (lo <= hi) bm_set(bm + (int64_t)rr.tag * wp, lo - a, hi - a);
+      uint32_t* bmt = bm + (int64_t)__popc(tag_mask & ((1u << rr.tag) - 1u)) * wp;
+      int64_t k = rka[ri] + (i - rcnt[ri]);
+      const int64_t kend = k + (iend - i);
+      if (rr.kind != 0) {
+        for (; k < kend; ++k) {
+          int64_t lo, hi;
+          run_interval(rr, k, Gr, T, abase, fbase, bd, gd, tpb, &lo, &hi);
+          lo = max(lo - kbase, a);
+          hi = min(hi - kbase, b - 1);
+          if (lo <= hi) bm_set(bmt, lo - a, hi - a);
+        }
+        i = iend;
+        continue;
+      }
+      bm_lattice(bmt, &rr, k, kend - k, kbase + a, b - a, Gr.g, Gr.shift);
+      i = iend;
     }
   }
   // non-monotone runs: every element, clipped
-  for (int r = 0; r < nr; ++r) {
+  for (int r = 0; r < (nonmono ? nr : 0); ++r) {
     if (rka[r] >= 0) continue;
     const Run& rr = druns[r];
     for (int64_t k = threadIdx.x; k < rr.count; k += kNT) {
@@ -647,13 +1059,59 @@ __device__ void bitmap_range(uint32_t* bm, const Run* druns, const int64_t* rcnt
       run_interval(rr, k, Gr, T, abase, fbase, bd, gd, tpb, &lo, &hi);
       lo = max(lo - kbase, a);
       hi = min(hi - kbase, b - 1);
-      if (lo <= hi) bm_set(bm + (int64_t)rr.tag * wp, lo - a, hi - a);
+      if (lo <= hi) bm_set(bm + (int64_t)__popc(tag_mask & ((1u << rr.tag) - 1u)) * wp, lo - a, hi - a);
     }
   }
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kPcSub = 16, kPcTags = 8;
+  if (U.n_sub <= kPcSub && n_tags <= kPcTags) {
+    // every requested measure in one pass over the words
+    if (threadIdx.x < U.n_sub) {
+      uint32_t cmq = 0;
+      for (uint32_t m = U.sub_mask[threadIdx.x] & tag_mask; m; m &= m - 1)
+        cmq |= 1u << __popc(tag_mask & ((1u << (__ffs(m) - 1)) - 1u));
+      U.sub_cm[threadIdx.x] = cmq;
+    }
+    __syncthreads();
+    int32_t c[kPcSub];
+#pragma unroll
+    for (int q = 0; q < kPcSub; ++q) c[q] = 0;
+    for (int64_t i = threadIdx.x; i < wp; i += kNT) {
+      uint32_t tw[kPcTags];
+#pragma unroll
+      for (int t = 0; t < kPcTags; ++t) tw[t] = t < n_tags ? bm[(int64_t)t * wp + i] : 0u;
+#pragma unroll
+      for (int q = 0; q < kPcSub; ++q) {
+        if (q >= U.n_sub) break;
+        const uint32_t mask = U.sub_cm[q];
+        uint32_t v = 0;
+#pragma unroll
+        for (int t = 0; t < kPcTags; ++t) v |= ((mask >> t) & 1u) ? tw[t] : 0u;
+        const int r = (int)U.sub_r[q];
+        c[q] += __popc(r == 1 ? v : bm_lines(v, r));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kPcSub; ++q) {
+      if (q >= U.n_sub) break;
+      int32_t v = c[q];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) wmax[q * kNW + w] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < U.n_sub) {
+      int64_t t = 0;
+      for (int k = 0; k < kNW; ++k) t += wmax[threadIdx.x * kNW + k];
+      U.sub_val[threadIdx.x] = t;
+    }
+    __syncthreads();
+    return;
+  }
   for (int q = 0; q < U.n_sub; ++q) {
-    const uint32_t mask = U.sub_mask[q];
+    uint32_t mask = 0;
+    for (uint32_t m = U.sub_mask[q] & tag_mask; m; m &= m - 1)
+      mask |= 1u << __popc(tag_mask & ((1u << (__ffs(m) - 1)) - 1u));
     const int r = (int)U.sub_r[q];
     int64_t c = 0;
     for (int64_t i = threadIdx.x; i < wp; i += kNT) {
@@ -703,6 +1161,7 @@ struct SetsArgs {
   int64_t n_warp_items;
   SplitState* split;        // key-range splitting of oversized units (may be null)
   int64_t sm_cap;           // test hook: cap on shared-memory elements (0 = none)
+  int32_t seg_off;          // A/B hook: no segment cover
   int32_t epoch;            // launch number; queue slots are ready when ready == epoch
 };
 
@@ -722,6 +1181,9 @@ struct MicroCnt {
 };
 constexpr int kMicroBytes = (int)(((sizeof(MicroCnt) + 15) & ~15) + (kMicroRuns + 1) * 8 + kMicroElems * 8);
 
+static_assert(kMicroElems * 8 >= kSegScratch, "segment scratch in the micro element buffer");
+static_assert(kNW * 256 * 4 + 256 * 4 + kMaxSub * kNW * 8 + (kSmemRuns + 1) * 8 + kSmemRuns * 8 >= kNW * kSegScratch,
+              "segment scratch in the sort/sweep region");
 static_assert(((sizeof(UnitSh) + 15) & ~size_t(15)) + kNW * kClassPts * 8 + (size_t)kNW * kMicroBytes <=
                   (size_t)kSetsSmemBytes,
               "micro tier does not fit the set kernel's shared memory");
@@ -766,6 +1228,7 @@ __device__ bool micro_unit(const SetsArgs& P, int64_t bidx, uint8_t* reg, int64_
   const int64_t gd[3] = {cfg.grid[0], cfg.grid[1], cfg.grid[2]};
   const int64_t* crow = P.coefs + c * (int64_t)P.T.max_acc * 8;
   const int64_t blk = G.sample_lin[j];
+  SegScratch* seg = reinterpret_cast<SegScratch*>(el);  // free until the intervals are emitted
   if (lane == 0) {
     cnt->n_runs = 0;
     cnt->status = GVO_OK;
@@ -812,7 +1275,8 @@ __device__ bool micro_unit(const SetsArgs& P, int64_t bidx, uint8_t* reg, int64_
         __syncwarp();
         for (int k = lane; k < m; k += 32) wpts[k] = (int64_t)((uint64_t)L0.base + (uint64_t)cp[p0 + k]);
         __syncwarp();
-        cover_warp(sink, L0, wpts, m, kind, Gr);
+        if (P.seg_off || !cover_segments(sink, L0, wpts, m, kind, Gr, seg))
+          cover_warp(sink, L0, wpts, m, kind, Gr);
       }
     }
   }
@@ -969,6 +1433,12 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
   __shared__ int fb_n, fb_i;
   __shared__ int64_t stat_idx;
   __shared__ long long t_runs_sh;
+  // debug phase accounting (thread 0): 0 fetch wait, 1 warp items, 2 micro
+  // bundles, 3 unit run building, 4 unit sort/sweep, 5 range counting,
+  // 6 range bitmap, 7 range emit/sort/sweep, 8 ranges, 9 bitmap ranges,
+  // 10 sum range N, 11 sum range runs
+  GVO_PH(__shared__ long long ph[16];)
+  GVO_PH(if (threadIdx.x < 16) ph[threadIdx.x] = 0;)
   if (threadIdx.x == 0) { main_done = 0; fb_n = 0; fb_i = 0; }
   // item space (mode 0): wave units | bundles of kNW block units (micro) | warp items;
   // block units falling back to the CTA path re-enter as kBlkBase + index
@@ -983,6 +1453,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
 
   for (;;) {
     // ---------------- fetch: queued key ranges first, then main items
+    const long long t_fetch = clock64();
     if (threadIdx.x == 0) {
       int kind = 2;
       int64_t it = -1;
@@ -1034,6 +1505,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
     __syncthreads();
     const int kind_fetched = next_kind;
     const int64_t item = next_item;
+    GVO_PH(if (threadIdx.x == 0) ph[0] += clock64() - t_fetch;)
     if (kind_fetched == 2) break;
 
     int64_t range_a = 0, range_b = 0;
@@ -1044,6 +1516,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
     if (!in_range && item >= n_set_main && item < kBlkBase) {
       warp_item(P.warp, item - n_set_main, reinterpret_cast<unsigned long long*>(ebuf));
       __syncthreads();
+      GVO_PH(if (threadIdx.x == 0) ph[1] += clock64() - t_start;)
       if (threadIdx.x == 0 && SS) atomicAdd(&SS->pending, ~0ull);
       continue;
     }
@@ -1088,6 +1561,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           us[6] = smid; us[7] = 0; us[8] = 3;
         }
       }
+      GVO_PH(if (threadIdx.x == 0) ph[2] += clock64() - t_start;)
       if (threadIdx.x == 0 && SS) atomicAdd(&SS->pending, ~0ull);
       continue;
     }
@@ -1265,6 +1739,8 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         const int ncl = max(ncl0, ncl1);
         const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
         int64_t* wpts = cpts + wid * kClassPts;
+        // hist .. rka are free while runs are built
+        SegScratch* seg = reinterpret_cast<SegScratch*>(micro_region + wid * kSegScratch);
         for (int task = wid; task < U.n_src * 5 * ncl; task += kNW) {
           const int s = task / (5 * ncl), rem = task % (5 * ncl), bi = rem / ncl, ci = rem % ncl;
           const int slot = slot0 + U.src_kind[s];
@@ -1283,13 +1759,15 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
             __syncwarp();
             for (int k = lane; k < m; k += 32) wpts[k] = (int64_t)((uint64_t)L0.base + (uint64_t)cp[p0 + k]);
             __syncwarp();
-            cover_warp(sink, L0, wpts, m, U.src_tag[s], Gr);
+            const bool segd = !P.seg_off && cover_segments(sink, L0, wpts, m, U.src_tag[s], Gr, seg);
+            if (!segd) cover_warp(sink, L0, wpts, m, U.src_tag[s], Gr);
+            GVO_PH(if (lane == 0) atomicAdd((unsigned long long*)&ph[segd ? 12 : 13], 1ull);)
           }
         }
       }
       __syncthreads();
 
-    if (threadIdx.x == 0) t_runs_sh = clock64();
+    if (threadIdx.x == 0) { t_runs_sh = clock64(); GVO_PH(ph[3] += t_runs_sh - t_start;) }
     // ---------------- offsets of runs, element count
       const int nr = min(U.n_runs, (int)P.run_cap);
       int64_t* roff = nr <= kSmemRuns ? roff_sh : roff_gl;
@@ -1315,6 +1793,8 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       if (threadIdx.x == 0) {
         const int64_t acc = roff[nr];
         U.N = acc;
+        GVO_PH(ph[14] += acc;)
+        GVO_PH(ph[15] += nr;)
         const int64_t base = floordiv(U.key_lo, U.R) * U.R;
         U.key_lo = base;
         if (U.status == GVO_OK) {
@@ -1345,7 +1825,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         __shared__ int64_t desc_off;
         if (threadIdx.x == 0) {
           const int64_t hb = (sizeof(SplitHdr) + 15) & ~int64_t(15);
-          const int64_t need = hb + (int64_t)nr * (int64_t)sizeof(Run);
+          const int64_t need = hb + (int64_t)nr * (int64_t)sizeof(Run) + 16 * (int64_t)nr;
           const unsigned long long o = atomicAdd(&SS->arena_top, (unsigned long long)need);
           desc_off = (int64_t)(o + need) <= SS->arena_bytes ? (int64_t)o : -1;
           if (desc_off >= 0) {
@@ -1358,15 +1838,43 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
             }
             h->outstanding = 1;
             h->status = GVO_OK;
+            h->tag_mask = 0;
           }
         }
         __syncthreads();
         if (desc_off >= 0) {
           Run* dr = reinterpret_cast<Run*>(SS->arena + desc_off + ((sizeof(SplitHdr) + 15) & ~size_t(15)));
-          for (int r = threadIdx.x; r < nr; r += kNT) dr[r] = runs[r];
+          int64_t* lim = reinterpret_cast<int64_t*>(dr + nr);  // [first, last] granule (relative) per run
+          SplitHdr* h = reinterpret_cast<SplitHdr*>(SS->arena + desc_off);
+          uint32_t tm = 0;
+          for (int r = threadIdx.x; r < nr; r += kNT) {
+            const Run rr = runs[r];
+            dr[r] = rr;
+            tm |= 1u << rr.tag;
+            int64_t lo = INT64_MIN, hi = INT64_MAX;  // points runs: unknown extent
+            if (rr.kind == 0) {
+              uint64_t ext = rr.span;
+              for (int d = 0; d < rr.nd; ++d) ext += (uint64_t)rr.stride[d] * (uint64_t)(rr.ext[d] - 1);
+              lo = Gr.of(rr.base) - U.key_lo;
+              hi = Gr.of((int64_t)((uint64_t)rr.base + ext)) - U.key_lo;
+            }
+            lim[2 * r] = lo;
+            lim[2 * r + 1] = hi;
+          }
+          tm = __reduce_or_sync(0xffffffffu, tm);
+          if ((threadIdx.x & 31) == 0 && tm) atomicOr(&h->tag_mask, tm);
           __threadfence();
           __syncthreads();
           hdr = reinterpret_cast<SplitHdr*>(SS->arena + desc_off);
+          if (threadIdx.x == 0 && P.unit_stats) {  // debug: split unit record
+            const unsigned long long slot =
+                atomicAdd(reinterpret_cast<unsigned long long*>(P.unit_stats + P.n_items * 10), 1ull);
+            if (slot < 4096) {
+              int64_t* us = P.unit_stats + P.n_items * 10 + 10 + slot * 10;
+              us[0] = U.field; us[1] = U.kind; us[2] = U.j; us[3] = U.N; us[4] = 0; us[5] = nr;
+              us[6] = U.key_hi - U.key_lo; us[7] = c; us[8] = 4;
+            }
+          }
           in_range = true;
           range_a = 0;
           range_b = ((U.key_hi - U.key_lo) / U.R + 1) * U.R;
@@ -1417,37 +1925,47 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       const int nr = hdr->nr;
       const Run* druns = reinterpret_cast<const Run*>(reinterpret_cast<const uint8_t*>(hdr) +
                                                       ((sizeof(SplitHdr) + 15) & ~size_t(15)));
+      const int64_t* dlim = reinterpret_cast<const int64_t*>(druns + nr);
+      const uint32_t tag_mask = *reinterpret_cast<volatile const uint32_t*>(&hdr->tag_mask);
       int64_t* rcnt = nr <= kSmemRuns ? roff_sh : roff_gl;
       int64_t* rka = nr <= kSmemRuns ? rka_sh : rka_gl;
       __shared__ int64_t s_N;
-      __shared__ int s_split, s_bm;
+      __shared__ int s_split, s_bm, s_nonmono;
       int64_t a = range_a, b = range_b;
-      // tags in use and whether every rescale divides a 32-bit word
-      int n_tags = 0;
+      const long long t_r0 = clock64();
+      // tags present in the runs (the bitmap keeps one plane per present
+      // tag) and whether every rescale divides a 32-bit word
+      const int n_tags = __popc(tag_mask);
       bool bm_r_ok = true;
-      for (int q = 0; q < U.n_sub; ++q) {
-        const uint32_t m = U.sub_mask[q];
-        if (m) n_tags = max(n_tags, 32 - __clz((int)m));
+      for (int q = 0; q < U.n_sub; ++q)
         bm_r_ok = bm_r_ok && U.sub_r[q] >= 1 && U.sub_r[q] <= 32 && (32 % U.sub_r[q]) == 0;
-      }
       const int64_t bm_words = sm_elems * 4;  // ebuf holds 2*sm_elems 8-byte elements
       for (;;) {
-        // count in-range elements per run (monotone runs: bisection)
+        // count in-range elements per run (monotone runs: closed form)
+        if (threadIdx.x == 0) s_nonmono = 0;
+        __syncthreads();
         for (int r = threadIdx.x; r < nr; r += kNT) {
+          const int64_t first = dlim[2 * r], last = dlim[2 * r + 1];
+          if (last < a || first >= b) {  // whole run outside [a, b)
+            rka[r] = 0;
+            rcnt[r] = 0;
+            continue;
+          }
           const Run& rr = druns[r];
           if (rr.kind == 0 && rr.mono) {
-            const int64_t ka = mono_first(rr, Gr, kbase, a, true);
-            const int64_t kb = mono_first(rr, Gr, kbase, b, false);
+            const int64_t ka = first >= a ? 0 : mono_first(rr, Gr, kbase, a, true);
+            const int64_t kb = last < b ? rr.count : mono_first(rr, Gr, kbase, b, false);
             rka[r] = ka;
             rcnt[r] = kb > ka ? kb - ka : 0;
           } else {
             rka[r] = -1;
             rcnt[r] = 0;
+            s_nonmono = 1;
           }
         }
         __syncthreads();
         // non-monotone runs: scan all their elements (rare)
-        for (int r = 0; r < nr; ++r) {
+        for (int r = 0; r < (s_nonmono ? nr : 0); ++r) {
           if (rka[r] >= 0) continue;
           const Run& rr = druns[r];
           int64_t local = 0;
@@ -1467,10 +1985,9 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           }
           __syncthreads();
         }
+        cta_scan_excl(rcnt, nr, wmax);
         if (threadIdx.x == 0) {
-          int64_t acc = 0;
-          for (int r = 0; r < nr; ++r) { const int64_t v = rcnt[r]; rcnt[r] = acc; acc += v; }
-          rcnt[nr] = acc;
+          const int64_t acc = rcnt[nr];
           s_N = acc;
           s_split = 0;
           // bitmap tier: one bit per granule and tag over [a, b) in the
@@ -1481,27 +1998,44 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           const bool bm_cheaper = acc * 96 > (int64_t)n_tags * wp * 2 + wp * 3 * (int64_t)U.n_sub;
           s_bm = bm_fit && (acc > sm_elems || bm_cheaper) ? 1 : 0;
           if (!s_bm && acc > sm_elems && b - a > R) {
-            const int64_t mid = a + ((b - a) / (2 * R)) * R;
-            if (mid > a && mid < b) {
-              atomicAdd(&hdr->outstanding, 1);
-              atomicAdd(&SS->pending, 1ull);
-              const unsigned long long slot = atomicAdd(&SS->qtail, 1ull);
-              if ((int64_t)slot < SS->q_cap) {
-                RangeItem it;
-                it.desc = (int64_t)(reinterpret_cast<uint8_t*>(hdr) - SS->arena);
-                it.a = mid;
-                it.b = b;
-                it.ready = 0;
-                it.pad = 0;
-                SS->queue[slot] = it;
-                __threadfence();
-                *reinterpret_cast<volatile int32_t*>(&SS->queue[slot].ready) = P.epoch;
-                s_split = 1;
-                b = mid;
-              } else {
-                atomicSub(&hdr->outstanding, 1);
-                atomicAdd(&SS->pending, ~0ull);
+            // split into pieces sized for the tier the density favours (one
+            // level instead of repeated halving); piece 0 is processed here
+            const double dens = (double)acc / (double)(b - a);
+            const bool bm_pref = bm_r_ok && n_tags > 0 && dens * 96.0 * 32.0 > 2.0 * n_tags + 3.0 * U.n_sub;
+            int64_t width = bm_pref ? (bm_words / n_tags) * 32
+                                    : (int64_t)((double)(b - a) * 0.8 * (double)sm_elems / (double)acc);
+            width = max(R, (width / R) * R);
+            int64_t m = (b - a + width - 1) / width;
+            if (m > 64) {
+              m = 64;
+              width = (((b - a) / 64) / R + 1) * R;
+              m = (b - a + width - 1) / width;
+            }
+            if (m > 1) {
+              atomicAdd(&hdr->outstanding, (int)(m - 1));
+              atomicAdd(&SS->pending, (unsigned long long)(m - 1));
+              const unsigned long long slot0 = atomicAdd(&SS->qtail, (unsigned long long)(m - 1));
+              const int64_t desc = (int64_t)(reinterpret_cast<uint8_t*>(hdr) - SS->arena);
+              for (int64_t t = 1; t < m; ++t) {
+                const unsigned long long slot = slot0 + (unsigned long long)(t - 1);
+                if ((int64_t)slot < SS->q_cap) {
+                  RangeItem it;
+                  it.desc = desc;
+                  it.a = a + t * width;
+                  it.b = min(b, a + (t + 1) * width);
+                  it.ready = 0;
+                  it.pad = 0;
+                  SS->queue[slot] = it;
+                  __threadfence();
+                  *reinterpret_cast<volatile int32_t*>(&SS->queue[slot].ready) = P.epoch;
+                } else {  // queue full: the piece is lost, the unit fails loudly
+                  atomicExch(&hdr->status, GVO_ERR_CAPACITY);
+                  atomicSub(&hdr->outstanding, 1);
+                  atomicAdd(&SS->pending, ~0ull);
+                }
               }
+              s_split = 1;
+              b = a + width;
             }
           }
           cur_range.a = a;
@@ -1512,16 +2046,19 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         if (!s_split) break;
       }
       const int64_t N = s_N;
+      const long long t_r1 = clock64();
+      GVO_PH(if (threadIdx.x == 0) { ph[5] += t_r1 - t_r0; ph[8] += 1; ph[9] += s_bm; ph[10] += N; ph[11] += nr; })
       if (s_bm) {
         bitmap_range(reinterpret_cast<uint32_t*>(ebuf), druns, rcnt, rka, nr, N, a, b, kbase, n_tags, Gr, P.T, abase,
-                     fbase, bd, gd, tpb, U, wmax);
+                     fbase, bd, gd, tpb, U, wmax, s_nonmono != 0, tag_mask);
         if (threadIdx.x < U.n_sub) atomicAdd(&hdr->acc[threadIdx.x], (unsigned long long)U.sub_val[threadIdx.x]);
+        GVO_PH(if (threadIdx.x == 0) ph[6] += clock64() - t_r1;)
       } else if (N > P.elem_cap) {
         if (threadIdx.x == 0) atomicExch(&hdr->status, GVO_ERR_CAPACITY);
       } else {
         uint64_t* A0 = N <= sm_elems ? ebuf : gbuf;
         uint64_t* B0 = N <= sm_elems ? ebuf + sm_elems : gbuf + P.elem_cap;
-        // emission (clipped to [a, b), keys relative to a)
+        // emission (clipped to [a, b), keys relative to a); dim 0 stepped
         {
           const int64_t per = (N + kNT - 1) / kNT;
           const int64_t e0 = min(N, (int64_t)threadIdx.x * per), e1 = min(N, e0 + per);
@@ -1534,20 +2071,42 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
             }
             ri = lo;
           }
-          for (int64_t i = e0; i < e1; ++i) {
+          int64_t i = e0;
+          while (i < e1) {
             while (rcnt[ri + 1] <= i) ++ri;
-            if (rka[ri] < 0) continue;  // non-monotone runs: compacted below
+            const int64_t iend = min(e1, rcnt[ri + 1]);
+            if (rka[ri] < 0) { i = iend; continue; }  // non-monotone runs: compacted below
             const Run& rr = druns[ri];
-            const int64_t k = rka[ri] + (i - rcnt[ri]);
-            int64_t lo, hi;
-            run_interval(rr, k, Gr, P.T, abase, fbase, bd, gd, tpb, &lo, &hi);
-            lo = max(lo - kbase, a);
-            hi = min(hi - kbase, b - 1);
-            A0[i] = ((uint64_t)(lo - a) << kKeyShift) | ((uint64_t)(hi - lo) << kTagBits) | (uint64_t)rr.tag;
+            const uint64_t tg = (uint64_t)rr.tag;
+            int64_t k = rka[ri] + (i - rcnt[ri]);
+            if (rr.kind != 0) {
+              for (; i < iend; ++i, ++k) {
+                int64_t lo, hi;
+                run_interval(rr, k, Gr, P.T, abase, fbase, bd, gd, tpb, &lo, &hi);
+                lo = max(lo - kbase, a);
+                hi = min(hi - kbase, b - 1);
+                A0[i] = ((uint64_t)(lo - a) << kKeyShift) | ((uint64_t)(hi - lo) << kTagBits) | tg;
+              }
+              continue;
+            }
+            const int nd = rr.nd;
+            const uint64_t st0 = nd ? (uint64_t)rr.stride[0] : 0;
+            const int64_t ex0 = nd ? rr.ext[0] : 1;
+            const uint64_t span = rr.span;
+            uint64_t bb = run_base(rr, k);
+            int64_t i0 = nd ? k % ex0 : 0;
+            for (; i < iend; ++i, ++k) {
+              int64_t lo = Gr.of((int64_t)bb) - kbase, hi = Gr.of((int64_t)(bb + span)) - kbase;
+              lo = max(lo, a);
+              hi = min(hi, b - 1);
+              A0[i] = ((uint64_t)(lo - a) << kKeyShift) | ((uint64_t)(hi - lo) << kTagBits) | tg;
+              if (++i0 < ex0) bb += st0;
+              else { i0 = 0; if (i + 1 < iend) bb = run_base(rr, k + 1); }
+            }
           }
         }
         __shared__ unsigned long long fillc;
-        for (int r = 0; r < nr; ++r) {
+        for (int r = 0; r < (s_nonmono ? nr : 0); ++r) {
           if (rka[r] >= 0) continue;
           if (threadIdx.x == 0) fillc = 0;
           __syncthreads();
@@ -1575,6 +2134,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         const uint64_t* sorted = cta_sort(A0, B0, N, kKeyShift, ((kb + 7) / 8) * 8, hist, tot);
         sweep(sorted, N, U, wmax);
         if (threadIdx.x < U.n_sub) atomicAdd(&hdr->acc[threadIdx.x], (unsigned long long)U.sub_val[threadIdx.x]);
+        GVO_PH(if (threadIdx.x == 0) ph[7] += clock64() - t_r1;)
       }
       if (threadIdx.x == 0 && P.unit_stats) {
         // range statistics after the unit slots: [idx][10]
@@ -1714,6 +2274,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       const long long t_sort = clock64();
       sweep(sorted, N, U, wmax);
       const long long t_sweep = clock64();
+      GVO_PH(if (threadIdx.x == 0) ph[4] += t_sweep - t_runs;)
 
       // ---------------- outputs
       if (threadIdx.x == 0 && P.unit_stats) {
@@ -1738,6 +2299,8 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       __syncthreads();
     }
   }
+  GVO_PH(if (P.unit_stats && threadIdx.x < 16 && blockIdx.x < 1024))
+    GVO_PH(P.unit_stats[P.n_items * 10 + 10 + 4096 * 10 + blockIdx.x * 16 + threadIdx.x] = ph[threadIdx.x];)
 }
 
 void launch_sets(const SetsLaunch& L, cudaStream_t st) {
@@ -1769,6 +2332,7 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st) {
   P.n_warp_items = L.n_warp_items;
   P.split = L.split;
   P.sm_cap = L.sm_cap;
+  P.seg_off = L.seg_off;
   static int32_t epoch = 0;
   P.epoch = ++epoch == 0 ? ++epoch : epoch;  // never 0 (the zeroed initial state)
   if (P.n_items + P.n_warp_items <= 0) return;

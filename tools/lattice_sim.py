@@ -193,3 +193,155 @@ if __name__ == "__main__":
           "non-mono intervals", sum(x[5] for x in r if not x[6]))
     for x in r[:40]:
         print(x)
+
+
+# ---------------------------------------------------------------- segments
+def decompose(L0, P):
+    """p - base0 = rho + sum_d k_d * s_d: round to nearest for d >= 1, floor for
+    dim 0 (rho in [0, s0))."""
+    base0, span0, dims0 = L0
+    out = []
+    for p in P:
+        off = p - base0
+        k = [0] * len(dims0)
+        for d in range(len(dims0) - 1, 0, -1):
+            s = dims0[d][0]
+            k[d] = (off + s // 2) // s
+            off -= k[d] * s
+        s0 = dims0[0][0]
+        k[0] = off // s0
+        off -= k[0] * s0
+        out.append((off, k))
+    return out
+
+
+def seg_ok(L0, P, g):
+    base0, span0, dims0 = L0
+    if not dims0 or len(P) < 2:
+        return False
+    s0 = dims0[0][0]
+    rs = sorted({r for r, _ in decompose(L0, P)})
+    tol = span0 + g
+    return all(b - a <= tol for a, b in zip(rs, rs[1:])) and rs[0] + s0 - rs[-1] <= tol
+
+
+def segment_cover(L0, P, g):
+    """Partition lattice-coordinate space by every translate's box boundaries;
+    in each segment box the present translates are fixed, their residues
+    cluster into spans (full cells fold into contiguous rows)."""
+    base0, span0, dims0 = L0
+    dec = decompose(L0, P)
+    nd = len(dims0)
+    bps = []
+    for d in range(nd):
+        e = dims0[d][1]
+        bps.append(sorted({k[d] for _, k in dec} | {k[d] + e for _, k in dec}))
+    import itertools
+    out = []
+    order = sorted(range(len(P)), key=lambda i: dec[i][0])
+    tol = span0 + g
+    for seg in itertools.product(*[range(len(b) - 1) for b in bps]):
+        lo = [bps[d][seg[d]] for d in range(nd)]
+        hi = [bps[d][seg[d] + 1] for d in range(nd)]
+        mem = [i for i in order
+               if all(dec[i][1][d] <= lo[d] and hi[d] <= dec[i][1][d] + dims0[d][1] for d in range(nd))]
+        if not mem:
+            continue
+        bS = base0 + sum(lo[d] * dims0[d][0] for d in range(nd))
+        dS = [(dims0[d][0], hi[d] - lo[d]) for d in range(nd)]
+        rs = [dec[i][0] for i in mem]
+        i = 0
+        while i < len(rs):
+            j = i
+            while j + 1 < len(rs) and rs[j + 1] - rs[j] <= tol:
+                j += 1
+            out.append(normalize(bS + rs[i], span0 + rs[j] - rs[i], dS, g))
+            i = j + 1
+    return out
+
+
+def granules(lats, g):
+    s = set()
+    for base, span, dims in lats:
+        idx = [np.arange(e) * st for st, e in dims]
+        b = np.array([base], dtype=np.int64)
+        for a in idx:
+            b = (b[:, None] + a[None, :]).ravel()
+        for bb in b.tolist():
+            s.update(range(bb // g, (bb + span) // g + 1))
+    return s
+
+
+def check_segments(k, machine, g=32, kind="block"):
+    """Brute-force exactness check of segment_cover against the translates."""
+    cs = coefs(k)
+    lc = k.launch
+    bd, gd = lc.block_dim, lc.grid_dim
+    total = gd[0] * gd[1] * gd[2]
+    srcs = [(total // 2, 1)] if kind == "block" else [(total // 2, 3)]
+    n_ok = n_seg = 0
+    for f in sorted({c[0] for c in cs}):
+        for kd in ("load", "store"):
+            classes = {}
+            for c in cs:
+                if c[0] == f and c[1] == kd:
+                    classes.setdefault(c[3], set()).add(c[2])
+            for s, cnt in srcs:
+                for box in run_boxes(s, cnt, gd):
+                    for cv, consts in classes.items():
+                        L0 = box_lattice(cv, bd, box, g)
+                        P = sorted(L0[0] + x for x in consts)
+                        truth = granules([(p, L0[1], L0[2]) for p in P], g)
+                        if seg_ok(L0, P, g):
+                            n_seg += 1
+                            got = granules(segment_cover(L0, P, g), g)
+                            assert got == truth, (f, kd, box)
+                        n_ok += 1
+    return n_ok, n_seg
+
+
+def unit_seg(k, machine, kind="wave", g=32):
+    """Interval count of a unit with and without the segment transform."""
+    cs = coefs(k)
+    lc = k.launch
+    bd, gd = lc.block_dim, lc.grid_dim
+    total = gd[0] * gd[1] * gd[2]
+    if kind == "wave":
+        per = blocks_per_wave(lc, machine)
+        nw = -(-total // per)
+        w = nw // 2
+        srcs = [(w * per, min(per, total - w * per))]
+    else:
+        srcs = [(total // 2, 1)]
+    old = new = nl_old = nl_new = 0
+    for f in sorted({c[0] for c in cs}):
+        for kd in ("load", "store"):
+            classes = {}
+            for c in cs:
+                if c[0] == f and c[1] == kd:
+                    classes.setdefault(c[3], set()).add(c[2])
+            for s, cnt in srcs:
+                for box in run_boxes(s, cnt, gd):
+                    for cv, consts in classes.items():
+                        L0 = box_lattice(cv, bd, box, g)
+                        P = sorted(L0[0] + x for x in consts)
+                        a = cover(L0, P, g)
+                        b = segment_cover(L0, P, g) if seg_ok(L0, P, g) else a
+                        cnt_ = lambda ls: sum(int(np.prod([e for _, e in d])) if d else 1 for _, _, d in ls)
+                        old += cnt_(a); new += cnt_(b); nl_old += len(a); nl_new += len(b)
+    return old, new, nl_old, nl_new
+
+
+def split_count(lat):
+    """Runs emit_lattice produces for one lattice (monotone split <= 64)."""
+    base, span, dims = lat
+    reach = span
+    combos = 1
+    ns = 0
+    for d, (s, e) in enumerate(dims):
+        if d > 0 and s <= reach:
+            ns += 1
+            combos *= e
+        else:
+            reach += s * (e - 1)
+    return 1 if ns == 0 or combos > 64 else combos

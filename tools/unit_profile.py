@@ -12,6 +12,8 @@ ctx = _native.context()
 L = _native.lib()
 wl = sys.argv[1] if len(sys.argv) > 1 else "C2"
 sp, _, _ = bench.build_shard(wl, 0, 1)
+if len(sys.argv) > 2:  # key filter, e.g. "D3Q27/zyxf"
+    sp = sp.subset(np.array([i for i in range(len(sp)) if sys.argv[2] in sp.key(i)]))
 cfgs = sp.config_array(ctx)
 kept = [type("K", (), {"key": sp.key(i)})() for i in range(len(sp))]
 L.gvo_debug_units(ctx.h, 1, None, 0, None)
@@ -19,11 +21,11 @@ for _ in range(2):
     out = ctx.eval_configs_host(cfgs, 5, 2, 0)
 n_items = _native.C.c_int64()
 L.gvo_debug_units(ctx.h, 1, None, 0, _native.C.byref(n_items))
-raw = np.zeros(n_items.value * 10 + 10 + 4096 * 10, dtype=np.int64)
+raw = np.zeros(n_items.value * 10 + 10 + 4096 * 10 + 1024 * 16, dtype=np.int64)
 L.gvo_debug_units(ctx.h, 0, _native._ptr(raw), raw.size, None)
 st = raw[: n_items.value * 10].reshape(-1, 10)
 nrng = int(raw[n_items.value * 10])
-rng_rows = raw[n_items.value * 10 + 10: n_items.value * 10 + 10 + nrng * 10].reshape(-1, 10)
+rng_rows = raw[n_items.value * 10 + 10: n_items.value * 10 + 10 + min(nrng, 4096) * 10].reshape(-1, 10)
 F = out["F"]; S = out["S"]
 per_cfg = F * (S + 1)
 rows = []
@@ -53,6 +55,21 @@ if nrng:
     if bund:
         cyc = sorted(r[4] for r in bund)
         print("bundles", len(bund), "total Mcycles", sum(cyc) / 1e6, "p50", cyc[len(cyc)//2], "max", cyc[-1], "fallbacks", sum(r[2] for r in bund))
-    rr = sorted([r for r in rng_rows.tolist() if r[8] != 3], key=lambda r: -r[4])
+    su = [r for r in rng_rows.tolist() if r[8] == 4]
+    if su:
+        su.sort(key=lambda r: -r[3])
+        print("split units", len(su), "sum N", sum(r[3] for r in su))
+        for r in su[:25]:
+            print("  split", kept[r[7]].key, "field", r[0], "kind", r[1], "N", r[3], "nr", r[5], "span", r[6])
+    rr = sorted([r for r in rng_rows.tolist() if r[8] not in (3, 4)], key=lambda r: -r[4])
     print("range cycles total M", sum(r[4] for r in rr) / 1e6, "max", rr[0][4])
     for r in rr[:15]: print("desc", r[0], "a", r[1], "b", r[2], "N", r[3], "cyc", r[4], "nr", r[5], "sm", r[6], "cfg", kept[r[7]].key, "queued" if r[8] == 1 else "first")
+# per-CTA phase accounting (k_sets debug counters)
+base = n_items.value * 10 + 10 + 4096 * 10
+ph = raw[base: base + 1024 * 16].reshape(1024, 16)
+ph = ph[ph.sum(1) != 0]
+names = ["fetch-wait", "warp-items", "micro", "unit-runs", "unit-sort/sweep", "range-count", "range-bitmap",
+         "range-emit/sort/sweep"]
+tot = ph[:, :8].sum(0) / 1e6
+print("CTAs", len(ph), "phase Gcycles (sum over CTAs):", {n: round(v / 1e3, 3) for n, v in zip(names, tot)})
+print("ranges", int(ph[:, 8].sum()), "bitmap", int(ph[:, 9].sum()), "sum N", int(ph[:, 10].sum()), "sum nr", int(ph[:, 11].sum()), "seg ok", int(ph[:, 12].sum()), "seg no", int(ph[:, 13].sum()), "unit N", int(ph[:, 14].sum()), "unit runs", int(ph[:, 15].sum()))
