@@ -15,7 +15,10 @@ from pathlib import Path
 import numpy as np
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / ("libgvo_b200_prof.so" if os.environ.get("GVO_LIB_VARIANT") == "prof" else "libgvo_b200.so")
+# GVO_LIB_VARIANT=<name> loads a variant build (libgvo_b200_<name>.so: the
+# phase-counter build "prof" or an A/B experiment); default: the product
+_VARIANT = os.environ.get("GVO_LIB_VARIANT", "")
+LIB_PATH = _HERE / (f"libgvo_b200_{_VARIANT}.so" if _VARIANT else "libgvo_b200.so")
 
 GVO_MAX_FIELDS = 16
 GVO_MAX_ACCESSES = 1024

@@ -18,7 +18,8 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 # GVO_BUILD_VARIANT=prof: same sources with the set kernel's per-CTA phase
-# counters compiled in (tools/unit_profile.py), as a separate library
+# counters compiled in (tools/unit_profile.py), as a separate library; other
+# variant names take extra -D flags from GVO_BUILD_DEFS (A/B experiments)
 VARIANT = os.environ.get("GVO_BUILD_VARIANT", "")
 OBJ = HERE / "build" / ("obj_" + VARIANT if VARIANT else "obj")
 LIB = HERE / ("libgvo_b200_" + VARIANT + ".so" if VARIANT else "libgvo_b200.so")
@@ -26,7 +27,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                 "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr"] + (
-                    ["-DGVO_PHASE_STATS=1"] if VARIANT == "prof" else [])
+                    ["-DGVO_PHASE_STATS=1"] if VARIANT == "prof" else []) + os.environ.get("GVO_BUILD_DEFS", "").split()
 
 
 def _headers():

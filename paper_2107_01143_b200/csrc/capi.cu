@@ -96,6 +96,7 @@ struct gvo_ctx {
   int64_t split_qcap = 1 << 22, split_arena = 4096ll << 20;
   int64_t sm_cap = 0;  // GVO_SMEM_ELEMS test hook
   int32_t seg_off = 0; // GVO_SEG=0 disables the segment cover (A/B hook)
+  int32_t fuse_warp = 1; // GVO_FUSE_WARP=0: warp statistics as their own launch
   DBuf<uint8_t> rank_scratch;
   // host-variant staging
   DBuf<gvo_config> s_cfgs;
@@ -162,9 +163,11 @@ int gvo_open(int device, gvo_ctx** out) {
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return GVO_ERR_CUDA; }
   if (const char* e = getenv("GVO_ELEM_CAP")) ctx->elem_cap = atoll(e);
   if (const char* e = getenv("GVO_RUN_CAP")) ctx->run_cap = atoll(e);
+  if (const char* e = getenv("GVO_SPLIT_ARENA_MB")) ctx->split_arena = atoll(e) << 20;
   if (const char* e = getenv("GVO_BATCH")) ctx->batch = atoll(e);
   if (const char* e = getenv("GVO_SMEM_ELEMS")) ctx->sm_cap = atoll(e);
   if (const char* e = getenv("GVO_SEG")) ctx->seg_off = atoi(e) == 0;
+  if (const char* e = getenv("GVO_FUSE_WARP")) ctx->fuse_warp = atoi(e) != 0;
   ctx->n_ctas = kSetsCtasPerSm * ctx->n_sm;
   *out = ctx;
   return GVO_OK;
@@ -375,7 +378,7 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     WarpArgs WA{ctx->view, ctx->d_machines.p, cf, ctx->geos.p, ctx->coefs.p, nb * (S + 1), S, m0.sector_bytes,
                m0.bank_width_bytes, m0.l1_banks, 0, nullptr, cnt, stride, F,
                d_l1_access ? d_l1_access + b0 * l1_stride * 3 : nullptr, l1_stride, nullptr};
-    const bool fuse = (int64_t)warp_item_smem(ctx->max_acc) <= sets_ebuf_bytes();
+    const bool fuse = ctx->fuse_warp && (int64_t)warp_item_smem(ctx->max_acc) <= sets_ebuf_bytes();
     if (!fuse) {
       tmark_begin(ctx, 1, st, &tb);
       launch_warp(ctx->view, ctx->d_machines.p, cf, ctx->geos.p, ctx->coefs.p, nb * (S + 1), S, m0.sector_bytes,

@@ -14,6 +14,16 @@
 // A hardware warp evaluates exactly one modelled warp: lane i computes the
 // address of thread 32*w + i, so dedup is a register-level __match_any_sync
 // on the 64-bit granule, no shared memory traffic.
+//
+// Translation dedup: two affine accesses with the same coefficient vector
+// differ by a constant K (incl. the block terms).  The distinct granules of a
+// warp depend only on K mod g, and its bank wavefronts only on
+// K mod (bank width * banks): shifting every address by a multiple of the
+// modulus shifts every id by a whole number of granules / bank rounds.  So
+// per item the accesses are grouped by (field, kind, coefficients, residue)
+// and only one access per group is evaluated per modelled warp, weighted by
+// the group's summed multiplicity (stencil loads: 25 accesses -> 4 groups
+// for sectors, 9 for banks).
 #pragma once
 #include "gvo_bytecode.cuh"
 
@@ -56,13 +66,16 @@ struct WarpArgs {
   unsigned long long* out_totals;
 };
 
-// shared memory words needed for max_acc accesses
+constexpr int kWarpDedupAcc = 256;   // grouping is quadratic in the access count: off beyond
+
+// shared memory bytes needed for max_acc accesses: accumulators, coefficient
+// rows, group multiplicities (int64), group representative and key list
 __host__ __device__ inline size_t warp_item_smem(int max_acc) {
-  return (2 * kMaxFields + 11 * (size_t)max_acc) * sizeof(unsigned long long);
+  return (2 * kMaxFields + 14 * (size_t)max_acc) * sizeof(unsigned long long) + 3 * (size_t)max_acc * sizeof(int32_t);
 }
 
 // One item, all threads of the CTA (blockDim.x multiple of 32).
-__device__ inline void warp_item(const WarpArgs& W, int64_t item, unsigned long long* sh) {
+static __device__ __noinline__ void warp_item(const WarpArgs& W, int64_t item, unsigned long long* sh) {
   const TplView& T = W.T;
   const gvo_machine* machines = W.machines;
   const gvo_config* cfgs = W.cfgs;
@@ -123,24 +136,91 @@ __device__ inline void warp_item(const WarpArgs& W, int64_t item, unsigned long 
     // stage this config's coefficient rows (8 x int64 per access) in shared memory
     int64_t* scoef = reinterpret_cast<int64_t*>(acc_l1 + 3 * A);
     for (int i = threadIdx.x; i < 8 * A; i += blockDim.x) scoef[i] = crow[i];
+    int64_t* msum = scoef + 8 * A;                          // group multiplicity, by key index
+    uint64_t* fp = reinterpret_cast<uint64_t*>(msum + A);    // group fingerprint, by access
+    int64_t* kres = reinterpret_cast<int64_t*>(fp + A);      // constant residue, by access
+    int32_t* rep = reinterpret_cast<int32_t*>(kres + A);     // group representative, by access
+    int32_t* keys = rep + A;                                 // representatives in access order
+    int32_t* kidx = keys + A;                                // key index of a representative
+    const bool dedup = A <= kWarpDedupAcc;
     uint32_t skip_field = 0;  // fields whose sample is a translate of an earlier one
     if (mode == 0 && !is_l1)
       for (int f = 0; f < kMaxFields; ++f) skip_field |= (geos[c].dup_of[f][j] >= 0 ? 1u : 0u) << f;
     __syncthreads();
+    // group of each access: first access of the same field, kind and
+    // coefficients whose constant (block terms included) has the same residue
+    const int64_t modulus = is_l1 ? bw * nbk : sec;
+    for (int a = threadIdx.x; a < A; a += blockDim.x) {
+      const int64_t* ca = scoef + a * 8;
+      const int ga = abase + a;
+      uint64_t h = ~(uint64_t)a;  // unique: never grouped
+      int64_t ra = 0;
+      if (dedup && ca[7] == kAffine && modulus > 0) {
+        const int64_t ka = (int64_t)((uint64_t)ca[0] + (uint64_t)ca[4] * (uint64_t)bc[0] +
+                                     (uint64_t)ca[5] * (uint64_t)bc[1] + (uint64_t)ca[6] * (uint64_t)bc[2]);
+        ra = floormod(ka, modulus);
+        h = 0x9e3779b97f4a7c15ull * (uint64_t)(T.acc_field[ga] * 2 + T.acc_kind[ga] + 1);
+        for (int k = 1; k <= 6; ++k) h = (h ^ (uint64_t)ca[k]) * 0xff51afd7ed558ccdull;
+        h = ((h ^ (uint64_t)ra) * 0xc4ceb9fe1a85ec53ull) & ~(uint64_t(1) << 63);  // top bit clear
+      }
+      fp[a] = h;
+      kres[a] = ra;
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < A; a += blockDim.x) {
+      int r = a;
+      const uint64_t h = fp[a];
+      if (!(h >> 63)) {
+        const int64_t* ca = scoef + a * 8;
+        const int ga = abase + a;
+        for (int b = 0; b < a; ++b) {
+          if (fp[b] != h) continue;
+          const int64_t* cb = scoef + b * 8;
+          const int gb = abase + b;
+          if (cb[1] == ca[1] && cb[2] == ca[2] && cb[3] == ca[3] && cb[4] == ca[4] && cb[5] == ca[5] &&
+              cb[6] == ca[6] && T.acc_field[gb] == T.acc_field[ga] && T.acc_kind[gb] == T.acc_kind[ga] &&
+              kres[b] == kres[a]) {
+            r = b;
+            break;
+          }
+        }
+      }
+      rep[a] = r;
+    }
+    __syncthreads();
+    __shared__ int n_keys;
+    if (wid == 0) {  // representatives compacted in access order
+      int base = 0;
+      for (int a0 = 0; a0 < A; a0 += 32) {
+        const int a = a0 + lane;
+        const bool isk = a < A && rep[a] == a;
+        const unsigned bal = __ballot_sync(0xffffffffu, isk);
+        const int pos = base + __popc(bal & ((1u << lane) - 1u));
+        if (isk) { keys[pos] = a; msum[pos] = 0; kidx[a] = pos; }
+        base += __popc(bal);
+      }
+      if (lane == 0) n_keys = base;
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < A; a += blockDim.x)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&msum[kidx[rep[a]]]), (unsigned long long)T.acc_mult[abase + a]);
+    __syncthreads();
+    const int NK = n_keys;
 
-    // each hardware warp owns a contiguous range of (modelled warp, access)
+    // each hardware warp owns a contiguous range of (modelled warp, group)
     // tasks, so thread coordinates are recomputed only when the warp changes
-    const int64_t ntask = nw * A;
+    const int64_t ntask = nw * NK;
     const int64_t per = (ntask + nwarps - 1) / nwarps;
     const int64_t t0 = wid * per, t1 = min(ntask, t0 + per);
-    int64_t w = t0 / A;
-    int a = (int)(t0 - w * A);
+    int64_t w = NK ? t0 / NK : 0;
+    int ki = (int)(t0 - w * NK);
     int64_t crd[6];
     bool act = false;
     unsigned am = 0;
     bool fresh = true;
-    for (int64_t t = t0; t < t1; ++t, ++a) {
-      if (a == A) { a = 0; ++w; fresh = true; }
+    for (int64_t t = t0; t < t1; ++t, ++ki) {
+      if (ki == NK) { ki = 0; ++w; fresh = true; }
+      const int a = keys[ki];
       if (fresh) {
         fresh = false;
         const int64_t th = w * 32 + lane;
@@ -175,7 +255,7 @@ __device__ inline void warp_item(const WarpArgs& W, int64_t item, unsigned long 
       if (!is_l1) {
         if (lane == 0) {
           const int slot = fa * 2 + T.acc_kind[ga];
-          atomicAdd(&acc_fk[slot], (unsigned long long)(T.acc_mult[ga] * distinct));
+          atomicAdd(&acc_fk[slot], (unsigned long long)(msum[ki] * distinct));
         }
         continue;
       }
@@ -212,6 +292,16 @@ __device__ inline void warp_item(const WarpArgs& W, int64_t item, unsigned long 
         atomicAdd(&acc_l1[3 * a + 2], 1ull);
       }
     }
+    __syncthreads();
+    // group members take their representative's per-access L1 numbers
+    if (is_l1)
+      for (int a = threadIdx.x; a < A; a += blockDim.x)
+        if (rep[a] >= 0) {
+          const int r = rep[a];  // the representative's access index
+          acc_l1[3 * a + 0] = acc_l1[3 * r + 0];
+          acc_l1[3 * a + 1] = acc_l1[3 * r + 1];
+          acc_l1[3 * a + 2] = acc_l1[3 * r + 2];
+        }
     __syncthreads();
     if (mode == 0) {
       int64_t* row = counts + c * counts_stride;

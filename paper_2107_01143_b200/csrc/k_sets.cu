@@ -33,6 +33,17 @@ namespace gvo {
 #define GVO_PH(...)
 #endif
 
+// out-of-line set-engine stages (own register allocation, fewer spills in
+// the monolithic kernel); GVO_HOT_NOINLINE=0 inlines them (A/B builds)
+#ifndef GVO_HOT_NOINLINE
+#define GVO_HOT_NOINLINE 1
+#endif
+#if GVO_HOT_NOINLINE
+#define GVO_NOINL __noinline__
+#else
+#define GVO_NOINL
+#endif
+
 constexpr int kNT = 512;           // threads per CTA
 constexpr int kNW = kNT / 32;
 constexpr int kMaxSrc = 64;        // sources per unit
@@ -224,7 +235,7 @@ __device__ inline void emit_normalized(const RunSink& S, const Lat& L, int tag, 
 // point starts or continues exactly one maximal ray along that stride), so
 // all rays of a dimension are judged in parallel against the points not yet
 // covered by larger-stride rays; the same greedy as cover_and_emit.
-__device__ __noinline__ void cover_warp(const RunSink& S, const Lat& L0, const int64_t* P, int n, int tag,
+__device__ GVO_NOINL void cover_warp(const RunSink& S, const Lat& L0, const int64_t* P, int n, int tag,
                            const Granule& G) {
   const int lane = threadIdx.x & 31;
   uint64_t req = n >= 64 ? ~0ull : ((1ull << n) - 1);
@@ -747,7 +758,7 @@ __device__ inline int64_t mono_first(const Run& r, const Granule& Gr, int64_t kb
 // ------------------------------------------------------------------ sort
 // CTA-wide stable LSD radix sort (8-bit digits) of packed 64-bit elements
 // on bits [bit0, bit0 + nbits).  a/b may live in shared or global memory.
-__device__ __noinline__ uint64_t* cta_sort(uint64_t* a, uint64_t* b, int64_t n, int bit0, int nbits,
+__device__ GVO_NOINL uint64_t* cta_sort(uint64_t* a, uint64_t* b, int64_t n, int bit0, int nbits,
                               uint32_t* hist /* kNW*256 */, uint32_t* tot /* 256 */) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t chunk = (((n + kNW - 1) / kNW) + 255) & ~int64_t(255);
@@ -835,7 +846,7 @@ __device__ __noinline__ uint64_t* cta_sort(uint64_t* a, uint64_t* b, int64_t n, 
 // give each lane the running maximum R before its sub-chunk.  Pass 2: a
 // sequential walk adds max(0, hi - max(lo - 1, R)) per selected interval.
 constexpr int kSubGroup = 4;
-__device__ __noinline__ void sweep(const uint64_t* e, int64_t n, UnitSh& U, int64_t* wmax /* kMaxSub*kNW */) {
+__device__ GVO_NOINL void sweep(const uint64_t* e, int64_t n, UnitSh& U, int64_t* wmax /* kMaxSub*kNW */) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t chunk = (n + kNW - 1) / kNW;
   const int64_t beg = min(n, (int64_t)w * chunk), end = min(n, beg + chunk);
@@ -1848,7 +1859,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           SplitHdr* h = reinterpret_cast<SplitHdr*>(SS->arena + desc_off);
           uint32_t tm = 0;
           for (int r = threadIdx.x; r < nr; r += kNT) {
-            const Run rr = runs[r];
+            const Run& rr = runs[r];
             dr[r] = rr;
             tm |= 1u << rr.tag;
             int64_t lo = INT64_MIN, hi = INT64_MAX;  // points runs: unknown extent

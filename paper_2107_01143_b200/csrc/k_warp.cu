@@ -6,7 +6,7 @@
 
 namespace gvo {
 
-__global__ void __launch_bounds__(256) k_warp(WarpArgs W) {
+__global__ void __launch_bounds__(256, 4) k_warp(WarpArgs W) {
   extern __shared__ unsigned long long sh[];
   for (int64_t item = blockIdx.x; item < W.n_items; item += gridDim.x) warp_item(W, item, sh);
 }
