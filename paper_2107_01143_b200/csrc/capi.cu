@@ -93,7 +93,7 @@ struct gvo_ctx {
   // key-range splitting state: header + queue + descriptor arena
   DBuf<uint8_t> split_mem;
   SplitState* split = nullptr;
-  int64_t split_qcap = 1 << 22, split_arena = 4096ll << 20;
+  int64_t split_qcap = 1 << 22;
   int64_t sm_cap = 0;  // GVO_SMEM_ELEMS test hook
   int32_t seg_off = 0; // GVO_SEG=0 disables the segment cover (A/B hook)
   int32_t fuse_warp = 1; // GVO_FUSE_WARP=0: warp statistics as their own launch
@@ -163,7 +163,6 @@ int gvo_open(int device, gvo_ctx** out) {
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return GVO_ERR_CUDA; }
   if (const char* e = getenv("GVO_ELEM_CAP")) ctx->elem_cap = atoll(e);
   if (const char* e = getenv("GVO_RUN_CAP")) ctx->run_cap = atoll(e);
-  if (const char* e = getenv("GVO_SPLIT_ARENA_MB")) ctx->split_arena = atoll(e) << 20;
   if (const char* e = getenv("GVO_BATCH")) ctx->batch = atoll(e);
   if (const char* e = getenv("GVO_SMEM_ELEMS")) ctx->sm_cap = atoll(e);
   if (const char* e = getenv("GVO_SEG")) ctx->seg_off = atoi(e) == 0;
@@ -325,13 +324,19 @@ static int ensure_work(gvo_ctx* ctx, int64_t n) {
   if (!ctx->split) {
     const size_t hdr = 256;
     const size_t qb = (size_t)ctx->split_qcap * sizeof(RangeItem);
-    if (!ctx->split_mem.ensure(hdr + qb + (size_t)ctx->split_arena)) return set_err(ctx, GVO_ERR_CUDA, "split alloc failed%s");
+    const size_t n_slots = (size_t)ctx->n_ctas * kSplitSlotsPerCta;
+    const size_t fb = (n_slots * sizeof(int32_t) + 255) & ~size_t(255);
+    const size_t slot_bytes = split_slot_bytes(ctx->run_cap);
+    if (!ctx->split_mem.ensure(hdr + qb + fb + n_slots * slot_bytes))
+      return set_err(ctx, GVO_ERR_CUDA, "split alloc failed%s");
     SplitState h{};
     h.q_cap = ctx->split_qcap;
-    h.arena_bytes = ctx->split_arena;
+    h.arena_bytes = (int64_t)(n_slots * slot_bytes);
     h.queue = reinterpret_cast<RangeItem*>(ctx->split_mem.p + hdr);
-    h.arena = ctx->split_mem.p + hdr + qb;
-    CK(cudaMemset(ctx->split_mem.p, 0, hdr + qb));
+    h.slot_busy = reinterpret_cast<int32_t*>(ctx->split_mem.p + hdr + qb);
+    h.arena = ctx->split_mem.p + hdr + qb + fb;
+    h.slot_bytes = (int64_t)slot_bytes;
+    CK(cudaMemset(ctx->split_mem.p, 0, hdr + qb + fb));
     CK(cudaMemcpy(ctx->split_mem.p, &h, sizeof h, cudaMemcpyHostToDevice));
     CK(cudaDeviceSynchronize());
     ctx->split = reinterpret_cast<SplitState*>(ctx->split_mem.p);

@@ -236,7 +236,7 @@ struct SplitHdr {
   int32_t outstanding;
   int32_t status;
   uint32_t tag_mask;  // tags present in the runs (bitmap tier: compact tags)
-  int32_t pad_;
+  int32_t slot;       // descriptor slot (freed when the last range completes)
 };
 struct RangeItem {
   int64_t desc;  // byte offset of the SplitHdr in the arena
@@ -244,11 +244,18 @@ struct RangeItem {
   int32_t ready;
   int32_t pad;
 };
+// Descriptors live in fixed slots, kSplitSlotsPerCta per CTA, each sized for
+// run_cap runs: a CTA only starts a unit that may split while one of its
+// slots is free, and the CTA that completes a descriptor's last range frees
+// its slot, so descriptor memory is bounded whatever the batch size.
+constexpr int kSplitSlotsPerCta = 4;
 struct SplitState {
   unsigned long long qhead, qtail, pending, arena_top;
   int64_t q_cap, arena_bytes;
   RangeItem* queue;
-  uint8_t* arena;
+  uint8_t* arena;        // n_ctas * kSplitSlotsPerCta slots of slot_bytes
+  int32_t* slot_busy;    // one flag per slot (0 free)
+  int64_t slot_bytes;
 };
 
 }  // namespace gvo

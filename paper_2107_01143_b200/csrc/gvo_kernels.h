@@ -59,6 +59,7 @@ struct SetsLaunch {
 int64_t sets_ebuf_bytes();
 void launch_sets(const SetsLaunch& L, cudaStream_t st);
 int64_t sets_slab_bytes(int64_t run_cap, int64_t elem_cap);
+int64_t split_slot_bytes(int64_t run_cap);
 
 // float assembly + prediction (k_assemble.cu)
 void launch_finish(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs,

@@ -1468,8 +1468,16 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
     if (threadIdx.x == 0) {
       int kind = 2;
       int64_t it = -1;
+      // a unit that may split needs one of this CTA's descriptor slots free
+      auto slot_free = [&]() {
+        if (!SS) return true;
+        const volatile int32_t* sb = SS->slot_busy + (int64_t)blockIdx.x * kSplitSlotsPerCta;
+        for (int q = 0; q < kSplitSlotsPerCta; ++q)
+          if (sb[q] == 0) return true;
+        return false;
+      };
       for (;;) {
-        if (fb_i < fb_n) {
+        if (fb_i < fb_n && slot_free()) {
           kind = 0;
           it = kBlkBase + fb_list[fb_i++];
           if (fb_i == fb_n) fb_i = fb_n = 0;
@@ -1497,16 +1505,24 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           }
         }
         if (!main_done) {
-          const unsigned long long m = atomicAdd(P.work, 1ull);
-          if ((int64_t)m < n_main) {
-            kind = 0;
-            it = (int64_t)m;
-            if (SS) atomicAdd(&SS->pending, 1ull);
-            break;
+          // wave units (mode 0) and custom units may split; bundles and warp
+          // items never do (the counter only grows, so a peek past the wave
+          // units stays past them)
+          const int64_t peek = (int64_t)vload(P.work);
+          const bool may_split = P.mode != 0 || peek < n_wave_u;
+          if (!may_split || slot_free()) {
+            const unsigned long long m = atomicAdd(P.work, 1ull);
+            if ((int64_t)m < n_main) {
+              kind = 0;
+              it = (int64_t)m;
+              if (SS) atomicAdd(&SS->pending, 1ull);
+              break;
+            }
+            main_done = 1;
           }
-          main_done = 1;
         }
-        if (!SS || (vload(&SS->pending) == 0 && vload(&SS->qhead) >= min(vload(&SS->qtail), (unsigned long long)SS->q_cap)))
+        if (!SS || (main_done && fb_n == 0 && vload(&SS->pending) == 0 &&
+                    vload(&SS->qhead) >= min(vload(&SS->qtail), (unsigned long long)SS->q_cap)))
           break;
         __nanosleep(256);
       }
@@ -1835,10 +1851,16 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       if (U.N > sm_elems && SS) {
         __shared__ int64_t desc_off;
         if (threadIdx.x == 0) {
-          const int64_t hb = (sizeof(SplitHdr) + 15) & ~int64_t(15);
-          const int64_t need = hb + (int64_t)nr * (int64_t)sizeof(Run) + 16 * (int64_t)nr;
-          const unsigned long long o = atomicAdd(&SS->arena_top, (unsigned long long)need);
-          desc_off = (int64_t)(o + need) <= SS->arena_bytes ? (int64_t)o : -1;
+          desc_off = -1;
+          int slot = -1;
+          for (int q = 0; q < kSplitSlotsPerCta && slot < 0; ++q) {
+            const int sq = (int)blockIdx.x * kSplitSlotsPerCta + q;
+            if (*reinterpret_cast<volatile int32_t*>(SS->slot_busy + sq) == 0) slot = sq;
+          }
+          if (slot >= 0 && nr <= P.run_cap) {
+            SS->slot_busy[slot] = 1;  // only this CTA claims its own slots
+            desc_off = (int64_t)slot * SS->slot_bytes;
+          }
           if (desc_off >= 0) {
             SplitHdr* h = reinterpret_cast<SplitHdr*>(SS->arena + desc_off);
             h->cfg = c; h->field = U.field; h->kind = U.kind; h->j = U.j; h->n_sub = U.n_sub; h->nr = nr;
@@ -1850,6 +1872,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
             h->outstanding = 1;
             h->status = GVO_OK;
             h->tag_mask = 0;
+            h->slot = slot;
           }
         }
         __syncthreads();
@@ -1891,7 +1914,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           range_b = ((U.key_hi - U.key_lo) / U.R + 1) * U.R;
         }
       }
-      if (!in_range && U.N > P.elem_cap) {  // split arena exhausted
+      if (!in_range && U.N > P.elem_cap) {  // no descriptor slot free and too big for the slab
         if (threadIdx.x == 0) {
           if (P.mode == 0) {
             int64_t* row = P.counts + c * P.counts_stride;
@@ -2149,8 +2172,6 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       }
       if (threadIdx.x == 0 && P.unit_stats) {
         // range statistics after the unit slots: [idx][10]
-        const unsigned long long ri = atomicAdd(&SS->arena_top, 0ull);  // keep ordering cheap
-        (void)ri;
         const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(P.unit_stats + P.n_items * 10), 1ull);
         if (slot < 4096) {
           int64_t* us = P.unit_stats + P.n_items * 10 + 10 + slot * 10;
@@ -2177,6 +2198,8 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
             write_unit_outputs(P, c, hdr->field, hdr->kind, hdr->j, hdr->n_uw,
                                reinterpret_cast<const volatile unsigned long long*>(hdr->acc));
           }
+          __threadfence();
+          atomicExch(SS->slot_busy + hdr->slot, 0);  // the descriptor is dead: its slot is free
         }
         atomicAdd(&SS->pending, ~0ull);
       }
@@ -2348,7 +2371,8 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st) {
   P.epoch = ++epoch == 0 ? ++epoch : epoch;  // never 0 (the zeroed initial state)
   if (P.n_items + P.n_warp_items <= 0) return;
   cudaMemsetAsync(P.work, 0, sizeof(unsigned long long), st);
-  if (P.split) cudaMemsetAsync(P.split, 0, 4 * sizeof(unsigned long long), st);  // head, tail, pending, arena_top
+  // head, tail, pending (descriptor slots are all free again when a launch ends)
+  if (P.split) cudaMemsetAsync(P.split, 0, 4 * sizeof(unsigned long long), st);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sets, cudaFuncAttributeMaxDynamicSharedMemorySize, kSetsSmemBytes);
@@ -2364,6 +2388,11 @@ int64_t sets_ebuf_bytes() {
   size_t off = (sizeof(UnitSh) + 15) & ~size_t(15);
   off += kNW * 256 * 4 + 256 * 4 + kMaxSub * kNW * 8 + (kSmemRuns + 1) * 8 + kNW * kClassPts * 8 + kSmemRuns * 8;
   return (int64_t)kSetsSmemBytes - (int64_t)off;
+}
+
+int64_t split_slot_bytes(int64_t run_cap) {
+  const int64_t hb = (sizeof(SplitHdr) + 15) & ~int64_t(15);
+  return (hb + run_cap * (int64_t)(sizeof(Run) + 16) + 255) & ~int64_t(255);
 }
 
 int64_t sets_slab_bytes(int64_t run_cap, int64_t elem_cap) {
