@@ -97,6 +97,8 @@ struct gvo_ctx {
   int64_t sm_cap = 0;  // GVO_SMEM_ELEMS test hook
   int32_t seg_off = 0; // GVO_SEG=0 disables the segment cover (A/B hook)
   int32_t fuse_warp = 1; // GVO_FUSE_WARP=0: warp statistics as their own launch
+  int64_t big_batch = 1024;  // batches of at least this many configs use the 1-CTA/SM set kernel (GVO_BIG_BATCH)
+  int32_t epoch = 0;     // set-kernel launch counter (queue readiness tag)
   DBuf<uint8_t> rank_scratch;
   // host-variant staging
   DBuf<gvo_config> s_cfgs;
@@ -167,7 +169,8 @@ int gvo_open(int device, gvo_ctx** out) {
   if (const char* e = getenv("GVO_SMEM_ELEMS")) ctx->sm_cap = atoll(e);
   if (const char* e = getenv("GVO_SEG")) ctx->seg_off = atoi(e) == 0;
   if (const char* e = getenv("GVO_FUSE_WARP")) ctx->fuse_warp = atoi(e) != 0;
-  ctx->n_ctas = kSetsCtasPerSm * ctx->n_sm;
+  if (const char* e = getenv("GVO_BIG_BATCH")) ctx->big_batch = atoll(e);
+  ctx->n_ctas = kMaxSetsCtasPerSm * ctx->n_sm;
   *out = ctx;
   return GVO_OK;
 }
@@ -383,7 +386,9 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     WarpArgs WA{ctx->view, ctx->d_machines.p, cf, ctx->geos.p, ctx->coefs.p, nb * (S + 1), S, m0.sector_bytes,
                m0.bank_width_bytes, m0.l1_banks, 0, nullptr, cnt, stride, F,
                d_l1_access ? d_l1_access + b0 * l1_stride * 3 : nullptr, l1_stride, nullptr};
-    const bool fuse = ctx->fuse_warp && (int64_t)warp_item_smem(ctx->max_acc) <= sets_ebuf_bytes();
+    const bool big = nb >= ctx->big_batch;
+    const bool fuse = ctx->fuse_warp &&
+                      (int64_t)warp_item_smem(ctx->max_acc) <= (big ? sets1::sets_ebuf_bytes() : sets2::sets_ebuf_bytes());
     if (!fuse) {
       tmark_begin(ctx, 1, st, &tb);
       launch_warp(ctx->view, ctx->d_machines.p, cf, ctx->geos.p, ctx->coefs.p, nb * (S + 1), S, m0.sector_bytes,
@@ -426,7 +431,14 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
       ctx->unit_items = L.n_items;
     }
     tmark_begin(ctx, 2, st, &tb);
-    launch_sets(L, st);
+    if (++ctx->epoch == 0) ++ctx->epoch;
+    L.epoch = ctx->epoch;
+    if (big) {
+      L.n_ctas = ctx->n_sm;
+      sets1::launch_sets(L, st);
+    } else {
+      sets2::launch_sets(L, st);
+    }
     tmark_end(ctx, 2, st, tb);
     tmark_begin(ctx, 3, st, &tb);
     launch_finish(ctx->view, ctx->d_machines.p, cf, ctx->geos.p, nb, S, W, F, cnt, stride,
@@ -556,7 +568,9 @@ int gvo_group_footprint(gvo_ctx* ctx, int32_t tpl, const int32_t block[3], const
   L.split = ctx->split;
     L.sm_cap = ctx->sm_cap;
     L.seg_off = ctx->seg_off;
-  launch_sets(L, st);
+  if (++ctx->epoch == 0) ++ctx->epoch;
+  L.epoch = ctx->epoch;
+  sets2::launch_sets(L, st);
   launch_warp(ctx->view, ctx->d_machines.p, ctx->s_cfgs.p, ctx->geos.p, ctx->coefs.p, (int64_t)blocks.size(), 0, granularity, 1, 1, 1,
               ctx->s_i64c.p, nullptr, 0, F, nullptr, 0, ctx->s_ull.p, ctx->max_acc, ctx->n_sm, st);
   CK(cudaGetLastError());
@@ -620,7 +634,9 @@ int gvo_group_sets(gvo_ctx* ctx, int32_t tpl, const int32_t block[3], const int6
   L.split = ctx->split;
     L.sm_cap = ctx->sm_cap;
     L.seg_off = ctx->seg_off;
-  launch_sets(L, st);
+  if (++ctx->epoch == 0) ++ctx->epoch;
+  L.epoch = ctx->epoch;
+  sets2::launch_sets(L, st);
   CK(cudaGetLastError());
   int status = 0;
   CK(cudaMemcpyAsync(h_out, ctx->s_counts.p, nout * 8, cudaMemcpyDeviceToHost, st));

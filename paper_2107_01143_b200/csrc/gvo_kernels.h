@@ -6,12 +6,12 @@
 
 namespace gvo {
 
-// set kernel residency: CTAs per SM and dynamic shared memory per CTA
-#ifndef GVO_SETS_CTAS_PER_SM
-#define GVO_SETS_CTAS_PER_SM 2
-#endif
-constexpr int kSetsCtasPerSm = GVO_SETS_CTAS_PER_SM;
-constexpr int kSetsSmemBytes = kSetsCtasPerSm == 1 ? 222 * 1024 : 110 * 1024;
+// The set kernel is built in two residencies (k_sets.cu, k_sets1.cu):
+// sets2 = 2 CTAs x 512 threads per SM (64 registers, 110 KB shared memory
+// each: latency hiding for small batches), sets1 = 1 CTA per SM (128
+// registers, 222 KB: no spills, 2x wider bitmap ranges and sort buffers for
+// throughput-bound batches).  kMaxSetsCtasPerSm sizes the per-CTA scratch.
+constexpr int kMaxSetsCtasPerSm = 2;
 
 void launch_setup(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs,
                   int64_t n, const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos, int64_t* d_ctabs,
@@ -55,9 +55,16 @@ struct SetsLaunch {
   SplitState* split = nullptr;
   int64_t sm_cap = 0;
   int32_t seg_off = 0;
+  int32_t epoch = 1;  // launch number, unique across both residencies (queue readiness tag)
 };
+namespace sets1 {
 int64_t sets_ebuf_bytes();
 void launch_sets(const SetsLaunch& L, cudaStream_t st);
+}
+namespace sets2 {
+int64_t sets_ebuf_bytes();
+void launch_sets(const SetsLaunch& L, cudaStream_t st);
+}
 int64_t sets_slab_bytes(int64_t run_cap, int64_t elem_cap);
 int64_t split_slot_bytes(int64_t run_cap);
 

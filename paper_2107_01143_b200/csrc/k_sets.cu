@@ -23,7 +23,21 @@
 #include "gvo_kernels.h"
 #include "gvo_warp.cuh"
 
+// residency of this build of the set kernel (k_sets1.cu includes this file
+// with 1); each residency lives in its own namespace
+#ifndef GVO_SETS_CTAS_PER_SM
+#define GVO_SETS_CTAS_PER_SM 2
+#endif
+#if GVO_SETS_CTAS_PER_SM == 1
+#define GVO_SETS_NS sets1
+#else
+#define GVO_SETS_NS sets2
+#endif
+
 namespace gvo {
+namespace GVO_SETS_NS {
+constexpr int kSetsCtasPerSm = GVO_SETS_CTAS_PER_SM;
+constexpr int kSetsSmemBytes = kSetsCtasPerSm == 1 ? 222 * 1024 : 110 * 1024;
 
 // per-CTA phase accounting for tools/unit_profile.py (build with
 // GVO_PHASE_STATS=1); compiled out of the product kernel
@@ -2367,8 +2381,7 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st) {
   P.split = L.split;
   P.sm_cap = L.sm_cap;
   P.seg_off = L.seg_off;
-  static int32_t epoch = 0;
-  P.epoch = ++epoch == 0 ? ++epoch : epoch;  // never 0 (the zeroed initial state)
+  P.epoch = L.epoch;  // never 0 (the zeroed initial state), unique per launch
   if (P.n_items + P.n_warp_items <= 0) return;
   cudaMemsetAsync(P.work, 0, sizeof(unsigned long long), st);
   // head, tail, pending (descriptor slots are all free again when a launch ends)
@@ -2390,6 +2403,9 @@ int64_t sets_ebuf_bytes() {
   return (int64_t)kSetsSmemBytes - (int64_t)off;
 }
 
+}  // namespace GVO_SETS_NS
+
+#if GVO_SETS_CTAS_PER_SM != 1
 int64_t split_slot_bytes(int64_t run_cap) {
   const int64_t hb = (sizeof(SplitHdr) + 15) & ~int64_t(15);
   return (hb + run_cap * (int64_t)(sizeof(Run) + 16) + 255) & ~int64_t(255);
@@ -2398,5 +2414,7 @@ int64_t split_slot_bytes(int64_t run_cap) {
 int64_t sets_slab_bytes(int64_t run_cap, int64_t elem_cap) {
   return ((run_cap * (int64_t)sizeof(Run) + 2 * (run_cap + 1) * 8 + 2 * elem_cap * 8) + 255) & ~int64_t(255);
 }
+
+#endif
 
 }  // namespace gvo
