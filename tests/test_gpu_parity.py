@@ -219,3 +219,55 @@ def test_split_ranges_forced_small_capacity():
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", *tests], env=env,
                        capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def _interleaved_kernel(rng):
+    """A field with Q interleaved 8-byte components per cell (zyxf layout), read
+    by pull loads q <- cell + c_q (c_q random neighbour offsets) and written in
+    place: the translate classes whose residues tile a cell, which the set
+    engine covers by segment boxes (k_sets.cu cover_segments)."""
+    Q = int(rng.choice([3, 5, 9, 15, 27]))
+    W, H, D = 16, 8, 6
+    block = [(4, 2, 1), (8, 1, 2), (2, 4, 3), (16, 2, 1), (1, 8, 2), (4, 4, 2)][rng.integers(0, 6)]
+    grid = (W // block[0], H // block[1], D // block[2])
+    fields = (gvo.Field("src", 8, (W * H * D * Q,), alignment=int(rng.choice([0, 8, 24]))),
+              gvo.Field("dst", 8, (W * H * D * Q,), alignment=0))
+    full = rng.integers(0, 3) > 0  # every component read (residues tile the cell)
+    comps = range(Q) if full else sorted(set(int(v) for v in rng.integers(0, Q, size=max(1, Q // 2))))
+    x = f"(tidx + bidx * {block[0]})"
+    y = f"(tidy + bidy * {block[1]})"
+    z = f"(tidz + bidz * {block[2]})"
+    acc = []
+    for q in comps:
+        dx, dy, dz = (int(v) for v in rng.integers(-1, 2, size=3))
+        text = f"src + ((({x} + {-dx}) * {Q} + {q}) + (({y} + {-dy}) * {W} + ({z} + {-dz}) * {W * H}) * {Q}) * 8"
+        acc.append(gvo.Access("src", "load", gvo.parse(text, fields=["src", "dst"]), 1))
+        text = f"dst + (({x} * {Q} + {q}) + ({y} * {W} + {z} * {W * H}) * {Q}) * 8"
+        acc.append(gvo.Access("dst", "store", gvo.parse(text, fields=["src", "dst"]), 1))
+    return gvo.KernelDescriptor(fields=fields, accesses=tuple(acc), launch=gvo.LaunchConfig(block, grid))
+
+
+def test_interleaved_translates_vs_oracle():
+    rng = np.random.default_rng(2107)
+    for i in range(60):
+        k = _interleaved_kernel(rng)
+        nb = k.launch.total_blocks
+        cnt = int(rng.integers(1, nb + 1))
+        start = int(rng.integers(0, nb - cnt + 1))
+        g = int(rng.choice([8, 24, 32, 128]))
+        grp = CollaborativeGroup(k.launch, np.arange(start, start + cnt, dtype=np.int64), "L2")
+        r = gvo.grid_iteration(k, grp, g)
+        got = {(f, kd): (c.unique_count, c.total_count) for (f, kd), c in r.per_field.items()}
+        assert got == ora.footprint(k, grp.block_linear, g), (i, k.launch, len(k.accesses) // 2)
+
+
+def test_interleaved_evaluations_vs_oracle():
+    rng = np.random.default_rng(143)
+    m = gvo.b200_preset()
+    for i in range(8):
+        k = _interleaved_kernel(rng)
+        ov = int(rng.choice([0, 3, 7]))
+        p = gvo.evaluate_kernel(k, m, override_blocks_per_wave=ov or None)
+        ev = ora.evaluate_kernel(k, m, override=ov or None)
+        assert p.glups == ev["glups"] and p.limiter == ev["limiter"], i
+        assert p.volumes.dram_load.v_down == ev["volumes"]["dram_load"]["down"], i
