@@ -83,54 +83,120 @@ __device__ void build_classes_cta(const TplView& T, int tpl, const int64_t* crow
     rep_of[a] = (int16_t)r;
   }
   __syncthreads();
-  for (int a = threadIdx.x; a < A; a += blockDim.x) {
-    int cnt = 0;
-    if (rep_of[a] == a)
-      for (int b = 0; b < A; ++b) cnt += rep_of[b] == a;
-    members[a] = (int16_t)cnt;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t ncls = 0, off = 0;
-    for (int slot = 0; slot < 2 * kMaxFields; ++slot) {
-      ct.slot_first()[slot] = ncls;
-      for (int q = fko[slot]; q < fko[slot + 1]; ++q) {
-        const int a = T.fk_list[q];
-        if (rep_of[a] != a) continue;
-        ct.rep()[ncls] = a;
-        ct.start()[ncls] = off;
-        ct.cnt()[ncls] = members[a];
-        off += members[a];
-        ++ncls;
-      }
+  // class numbering in slot order: class = position q of fk_list holding a
+  // representative; ranks by a warp-0 ballot scan over fk_list (which is
+  // grouped by slot), then per-class distinct-constant counts
+  __shared__ int s_ncls;
+  int16_t* qrank = members;  // exclusive rank of representative positions, by fk_list position
+  const int q0 = fko[0], q1 = fko[2 * kMaxFields];
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int base = 0;
+    for (int qq = q0; qq < q1; qq += 32) {
+      const int q = qq + lane;
+      const bool isr = q < q1 && rep_of[T.fk_list[q]] == T.fk_list[q];
+      const unsigned bal = __ballot_sync(0xffffffffu, isr);
+      if (q < q1) qrank[q - q0] = (int16_t)(base + __popc(bal & ((1u << lane) - 1u)));
+      base += __popc(bal);
     }
-    ct.slot_first()[2 * kMaxFields] = ncls;
+    if (lane == 0) s_ncls = base;
   }
   __syncthreads();
-  const int64_t ncls = ct.slot_first()[2 * kMaxFields];
-  for (int64_t c = threadIdx.x; c < ncls; c += blockDim.x) {
-    const int64_t r = ct.rep()[c];
-    const int slot = T.acc_field[abase + r] * 2 + T.acc_kind[abase + r];
-    int64_t* P = ct.pts() + ct.start()[c];
-    int64_t n = 0;
-    for (int q = fko[slot]; q < fko[slot + 1]; ++q) {
-      const int a = T.fk_list[q];
-      if (rep_of[a] != r) continue;
-      const int64_t v = crow[a * 8];
-      int64_t j = n;
-      bool dup = false;
-      while (j > 0 && P[j - 1] >= v) {
-        if (P[j - 1] == v) { dup = true; break; }
-        --j;
-      }
-      if (dup) continue;
-      for (int64_t m = n; m > j; --m) P[m] = P[m - 1];
-      P[j] = v;
-      ++n;
+  const int ncls = s_ncls;
+  for (int slot = threadIdx.x; slot <= 2 * kMaxFields; slot += blockDim.x) {
+    const int q = fko[slot];
+    ct.slot_first()[slot] = slot == 2 * kMaxFields ? ncls : (q < q1 ? qrank[q - q0] : ncls);
+  }
+  // class c = rank of its representative's fk_list position; member count
+  int32_t* nu_start = reinterpret_cast<int32_t*>(members + ((T.max_acc + 1) & ~1));  // non-unique offsets (4-byte aligned)
+  int32_t* n_uniq = nu_start + T.max_acc;
+  for (int q = q0 + (int)threadIdx.x; q < q1; q += blockDim.x) {
+    const int a = T.fk_list[q];
+    if (rep_of[a] != a) continue;
+    const int c = qrank[q - q0];
+    const int slot = T.acc_field[abase + a] * 2 + T.acc_kind[abase + a];
+    int m = 0;
+    for (int q2 = fko[slot]; q2 < fko[slot + 1]; ++q2) m += rep_of[T.fk_list[q2]] == a;
+    ct.rep()[c] = a;
+    nu_start[c] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // ncls <= A
+    int off = 0;
+    for (int c = 0; c < ncls; ++c) { const int m = nu_start[c]; nu_start[c] = off; off += m; }
+  }
+  __syncthreads();
+  // members placed at their rank (ties by position) in the scratch row:
+  // each class's constants sorted, duplicates adjacent
+  int64_t* tmp = ct.rep_of();
+  for (int q = q0 + (int)threadIdx.x; q < q1; q += blockDim.x) {
+    const int b = T.fk_list[q];
+    const int r = rep_of[b];
+    if (r < 0) continue;
+    const int slot = T.acc_field[abase + b] * 2 + T.acc_kind[abase + b];
+    const int64_t v = crow[b * 8];
+    int rank = 0, qr = -1;
+    for (int q2 = fko[slot]; q2 < fko[slot + 1]; ++q2) {
+      const int b2 = T.fk_list[q2];
+      if (b2 == r) qr = q2;
+      if (rep_of[b2] != r) continue;
+      const int64_t u = crow[b2 * 8];
+      rank += (u < v) || (u == v && q2 < q);
     }
-    ct.cnt()[c] = n;
+    tmp[nu_start[qrank[qr - q0]] + rank] = v;
   }
   __syncthreads();
+  // distinct constants: a sorted element is kept unless it equals its predecessor
+  for (int c = threadIdx.x; c < ncls; c += blockDim.x) {
+    const int a = (int)ct.rep()[c];
+    const int slot = T.acc_field[abase + a] * 2 + T.acc_kind[abase + a];
+    int m = 0;
+    for (int q2 = fko[slot]; q2 < fko[slot + 1]; ++q2) m += rep_of[T.fk_list[q2]] == a;
+    const int e0 = nu_start[c];
+    int u = 0;
+    for (int i = 0; i < m; ++i) u += (i == 0 || tmp[e0 + i] != tmp[e0 + i - 1]);
+    n_uniq[c] = u;
+    ct.cnt()[c] = u;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // class point offsets: exclusive scan of distinct counts
+    int64_t off = 0;
+    for (int c = 0; c < ncls; ++c) { ct.start()[c] = off; off += n_uniq[c]; }
+  }
+  __syncthreads();
+  // compact: the thread of sorted element i writes it if it starts a new value
+  for (int q = q0 + (int)threadIdx.x; q < q1; q += blockDim.x) {
+    // element index within the scratch row = q - q0 covers every member once
+    const int i = q - q0;
+    // class of element i: last class whose non-unique start <= i (member
+    // counts are positive, so starts are strictly increasing)
+    int lo = 0, hi = ncls - 1;
+    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (nu_start[mid] <= i) lo = mid; else hi = mid - 1; }
+    if (ncls == 0) continue;
+    const int c = lo;
+    const int e0 = nu_start[c];
+    const int e1 = c + 1 < ncls ? nu_start[c + 1] : -1;
+    if (e1 >= 0 && i >= e1) continue;
+    // elements beyond the last class (non-affine accesses) are not in any class
+    const int a = (int)ct.rep()[c];
+    if (e1 < 0) {
+      const int slot = T.acc_field[abase + a] * 2 + T.acc_kind[abase + a];
+      int m = 0;
+      for (int q2 = fko[slot]; q2 < fko[slot + 1]; ++q2) m += rep_of[T.fk_list[q2]] == a;
+      if (i >= e0 + m) continue;
+    }
+    if (i > e0 && tmp[i] == tmp[i - 1]) continue;
+    int u = 0;
+    for (int k = e0 + 1; k <= i; ++k) u += tmp[k] != tmp[k - 1];
+    ct.pts()[ct.start()[c] + u] = tmp[i];
+  }
+  __syncthreads();
+}
+
+// dynamic shared memory of the setup kernels: rep_of and qrank (int16), the
+// classes' non-unique offsets and distinct counts (int32)
+static size_t setup_smem(int max_acc) {
+  return (size_t)2 * (((max_acc + 1) & ~1) * sizeof(int16_t)) + 2 * (size_t)max_acc * sizeof(int32_t);
 }
 
 // evaluation-order key of a (phase, group, access) overflow failure
@@ -168,7 +234,7 @@ __global__ void __launch_bounds__(256) k_setup(TplView T, const gvo_machine* mac
     crow[a * 8 + 7] = flag;
   }
   __syncthreads();
-  build_classes_cta(T, tpl, crow, CTab{ctabs + c * ctab_stride(T.max_acc), T.max_acc}, sh16, sh16 + T.max_acc);
+  build_classes_cta(T, tpl, crow, CTab{ctabs + c * ctab_stride(T.max_acc), T.max_acc}, sh16, sh16 + ((T.max_acc + 1) & ~1));
 
   // ---- geometry (thread 0)
   if (threadIdx.x == 0) {
@@ -364,7 +430,7 @@ void launch_setup(const TplView& T, const gvo_machine* d_machines, const gvo_con
                   int64_t n, const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos, int64_t* d_ctabs,
                   cudaStream_t st) {
   if (n > 0)
-    k_setup<<<(unsigned)n, 256, 2 * T.max_acc * sizeof(int16_t), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs,
+    k_setup<<<(unsigned)n, 256, setup_smem(T.max_acc), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs,
                                                                        d_geos, d_ctabs);
 }
 
@@ -374,13 +440,13 @@ __global__ void k_classes_only(TplView T, const gvo_config* cfgs, int64_t n, con
   if (c >= n) return;
   extern __shared__ int16_t sh_rep2[];
   build_classes_cta(T, cfgs[c].template_id, coefs + c * (int64_t)T.max_acc * 8,
-                    CTab{ctabs + c * ctab_stride(T.max_acc), T.max_acc}, sh_rep2, sh_rep2 + T.max_acc);
+                    CTab{ctabs + c * ctab_stride(T.max_acc), T.max_acc}, sh_rep2, sh_rep2 + ((T.max_acc + 1) & ~1));
 }
 
 void launch_classes(const TplView& T, const gvo_config* d_cfgs, int64_t n, const int64_t* d_coefs,
                     int64_t* d_ctabs, cudaStream_t st) {
   if (n > 0)
-    k_classes_only<<<(unsigned)n, 128, 2 * T.max_acc * sizeof(int16_t), st>>>(T, d_cfgs, n, d_coefs, d_ctabs);
+    k_classes_only<<<(unsigned)n, 128, setup_smem(T.max_acc), st>>>(T, d_cfgs, n, d_coefs, d_ctabs);
 }
 
 }  // namespace gvo
