@@ -333,7 +333,8 @@ def run_device(args, rank, world):
                              "than enumeration. peak = measured INT32 issue rate (gvo_int_peak).",
                      "hbm": {"achieved": algo_bytes / (ms_step * 1e-3) / 1e9, "peak": 6531.3, "unit": "GB/s",
                              "frac": algo_bytes / (ms_step * 1e-3) / 1e9 / 6531.3},
-                     "traffic": _ncu_traffic()},
+                     "traffic": _ncu_traffic(),
+                     "hw": _ncu_hw()},
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }
@@ -395,6 +396,23 @@ def _ncu_traffic():
         v, u = d[k]
         tot += float(v) * scale.get(u, 1)
     return tot
+
+
+def _ncu_hw():
+    """Hardware utilisation of the same k_sets launch from the committed ncu
+    capture: issue slots, ALU pipe, shared-memory wavefronts (the counters the
+    north star names), or None."""
+    p = ROOT / "profiles" / "r01_ncu_k_sets.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    pick = {"issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "alu_pipe_pct": "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+            "smem_wavefronts_pct": "l1tex__data_pipe_lsu_wavefronts_mem_shared.avg.pct_of_peak_sustained_elapsed",
+            "dram_pct": "dram__throughput.avg.pct_of_peak_sustained_elapsed"}
+    out = {k: float(d[v][0]) for k, v in pick.items() if v in d}
+    out["source"] = "profiles/r01_ncu_k_sets.json (ncu --set full, C2 bench k_sets launch)"
+    return out
 
 
 def main():
