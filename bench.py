@@ -269,9 +269,13 @@ def run_device(args, rank, world):
     value = n_real * args.steps / (ms_max * 1e-3)
 
     # ---- e2e through the C ABI with host buffers (copies inside the region)
-    counts_h = np.zeros((n, stride), dtype=np.int64)
-    stats_h = np.zeros((n, _native.stats_len(F)), dtype=np.float64)
-    rec_h = np.zeros((n, _native.RECORD_LEN), dtype=np.float64)
+    # host buffers in pinned memory (the inputs a user stages for the DMA engines)
+    counts_h = torch.zeros((n, stride), dtype=torch.int64, pin_memory=True).numpy()
+    stats_h = torch.zeros((n, _native.stats_len(F)), dtype=torch.float64, pin_memory=True).numpy()
+    rec_h = torch.zeros((n, _native.RECORD_LEN), dtype=torch.float64, pin_memory=True).numpy()
+    cfg_pin = torch.empty(cfg_np.nbytes, dtype=torch.uint8, pin_memory=True).numpy()
+    cfg_pin[:] = cfg_np.view(np.uint8).reshape(-1)
+    cfg_np = cfg_pin.view(cfg_np.dtype).reshape(cfg_np.shape)
     e2e_steps = max(3, args.steps // 2)
     if world > 1:
         dist.barrier()

@@ -11,7 +11,11 @@ namespace gvo {
 // each: latency hiding for small batches), sets1 = 1 CTA per SM (128
 // registers, 222 KB: no spills, 2x wider bitmap ranges and sort buffers for
 // throughput-bound batches).  kMaxSetsCtasPerSm sizes the per-CTA scratch.
+#ifdef GVO_SETS2_CTAS
+constexpr int kMaxSetsCtasPerSm = GVO_SETS2_CTAS;
+#else
 constexpr int kMaxSetsCtasPerSm = 2;
+#endif
 
 void launch_setup(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs,
                   int64_t n, const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos, int64_t* d_ctabs,

@@ -36,8 +36,14 @@
 
 namespace gvo {
 namespace GVO_SETS_NS {
+// the small-batch residency's shape can be overridden for experiments
+// (GVO_SETS2_CTAS / GVO_SETS2_NT, e.g. 4 x 256)
+#if GVO_SETS_CTAS_PER_SM != 1 && defined(GVO_SETS2_CTAS)
+constexpr int kSetsCtasPerSm = GVO_SETS2_CTAS;
+#else
 constexpr int kSetsCtasPerSm = GVO_SETS_CTAS_PER_SM;
-constexpr int kSetsSmemBytes = kSetsCtasPerSm == 1 ? 222 * 1024 : 110 * 1024;
+#endif
+constexpr int kSetsSmemBytes = kSetsCtasPerSm == 1 ? 222 * 1024 : kSetsCtasPerSm == 2 ? 110 * 1024 : 54 * 1024;
 
 // per-CTA phase accounting for tools/unit_profile.py (build with
 // GVO_PHASE_STATS=1); compiled out of the product kernel
@@ -58,7 +64,11 @@ constexpr int kSetsSmemBytes = kSetsCtasPerSm == 1 ? 222 * 1024 : 110 * 1024;
 #define GVO_NOINL
 #endif
 
+#if GVO_SETS_CTAS_PER_SM != 1 && defined(GVO_SETS2_NT)
+constexpr int kNT = GVO_SETS2_NT;  // threads per CTA (experiment)
+#else
 constexpr int kNT = 512;           // threads per CTA
+#endif
 constexpr int kNW = kNT / 32;
 constexpr int kMaxSrc = 64;        // sources per unit
 constexpr int kMaxSub = 72;        // subsets per unit
