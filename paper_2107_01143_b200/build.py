@@ -35,9 +35,21 @@ def _headers():
         HERE.parent / "include" / "gvo_b200.h"]
 
 
+def _included_sources(src: Path) -> list:
+    """.cu files a translation unit #includes (k_sets1.cu includes k_sets.cu)."""
+    out = []
+    for line in src.read_text().splitlines():
+        line = line.strip()
+        if line.startswith("#include") and line.endswith('.cu"'):
+            dep = CSRC / line.split('"')[1]
+            if dep.exists():
+                out.append(dep)
+    return out
+
+
 def _compile(src: Path, verbose: bool) -> Path:
     obj = OBJ / (src.stem + ".o")
-    newest = max([src.stat().st_mtime] + [h.stat().st_mtime for h in _headers()])
+    newest = max([src.stat().st_mtime] + [h.stat().st_mtime for h in _headers() + _included_sources(src)])
     if obj.exists() and obj.stat().st_mtime >= newest:
         return obj
     cmd = [NVCC, *FLAGS, "-c", str(src), "-o", str(obj)]

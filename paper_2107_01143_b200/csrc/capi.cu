@@ -96,6 +96,7 @@ struct gvo_ctx {
   int64_t split_qcap = 1 << 22;
   int64_t sm_cap = 0;  // GVO_SMEM_ELEMS test hook
   int32_t seg_off = 0; // GVO_SEG=0 disables the segment cover (A/B hook)
+  int32_t pat_off = 0; // GVO_PATTERN=0 disables pattern runs (A/B hook)
   int32_t fuse_warp = 1; // GVO_FUSE_WARP=0: warp statistics as their own launch
   int64_t big_batch = 1024;  // batches of at least this many configs use the 1-CTA/SM set kernel (GVO_BIG_BATCH)
   int32_t epoch = 0;     // set-kernel launch counter (queue readiness tag)
@@ -168,6 +169,7 @@ int gvo_open(int device, gvo_ctx** out) {
   if (const char* e = getenv("GVO_BATCH")) ctx->batch = atoll(e);
   if (const char* e = getenv("GVO_SMEM_ELEMS")) ctx->sm_cap = atoll(e);
   if (const char* e = getenv("GVO_SEG")) ctx->seg_off = atoi(e) == 0;
+  if (const char* e = getenv("GVO_PATTERN")) ctx->pat_off = atoi(e) == 0;
   if (const char* e = getenv("GVO_FUSE_WARP")) ctx->fuse_warp = atoi(e) != 0;
   if (const char* e = getenv("GVO_BIG_BATCH")) ctx->big_batch = atoll(e);
   ctx->n_ctas = kMaxSetsCtasPerSm * ctx->n_sm;
@@ -420,6 +422,7 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     L.split = ctx->split;
     L.sm_cap = ctx->sm_cap;
     L.seg_off = ctx->seg_off;
+    L.pat_off = ctx->pat_off;
     if (fuse) {
       L.warp = WA;
       L.n_warp_items = WA.n_items;
@@ -568,6 +571,7 @@ int gvo_group_footprint(gvo_ctx* ctx, int32_t tpl, const int32_t block[3], const
   L.split = ctx->split;
     L.sm_cap = ctx->sm_cap;
     L.seg_off = ctx->seg_off;
+    L.pat_off = ctx->pat_off;
   if (++ctx->epoch == 0) ++ctx->epoch;
   L.epoch = ctx->epoch;
   sets2::launch_sets(L, st);
@@ -634,6 +638,7 @@ int gvo_group_sets(gvo_ctx* ctx, int32_t tpl, const int32_t block[3], const int6
   L.split = ctx->split;
     L.sm_cap = ctx->sm_cap;
     L.seg_off = ctx->seg_off;
+    L.pat_off = ctx->pat_off;
   if (++ctx->epoch == 0) ++ctx->epoch;
   L.epoch = ctx->epoch;
   sets2::launch_sets(L, st);

@@ -237,6 +237,8 @@ struct SplitHdr {
   int32_t status;
   uint32_t tag_mask;  // tags present in the runs (bitmap tier: compact tags)
   int32_t slot;       // descriptor slot (freed when the last range completes)
+  int32_t has_pattern;  // pattern runs present: every range takes the bitmap tier
+  int32_t pad2_;
 };
 struct RangeItem {
   int64_t desc;  // byte offset of the SplitHdr in the arena

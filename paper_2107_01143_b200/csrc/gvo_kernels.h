@@ -59,6 +59,7 @@ struct SetsLaunch {
   SplitState* split = nullptr;
   int64_t sm_cap = 0;
   int32_t seg_off = 0;
+  int32_t pat_off = 0;
   int32_t epoch = 1;  // launch number, unique across both residencies (queue readiness tag)
 };
 namespace sets1 {

@@ -94,6 +94,7 @@ struct UnitSh {
   int n_runs;
   int64_t key_lo, key_hi;  // granule bounds over all runs
   int64_t N;
+  int has_pattern;          // pattern runs present: bitmap tier only
 };
 
 // ------------------------------------------------------------------ lattice
@@ -164,6 +165,7 @@ struct RunSink {
   int* status;
   int64_t* key_lo;
   int64_t* key_hi;
+  int* has_pattern = nullptr;  // set when a pattern run is emitted (bitmap tier only)
 };
 
 __device__ inline void emit_normalized(const RunSink& S, const Lat& L, int tag, const Granule& G);
@@ -252,6 +254,78 @@ __device__ inline void emit_normalized(const RunSink& S, const Lat& L, int tag, 
   r->run_start = r->run_count = 0;
   atomicMin((long long*)S.key_lo, (long long)G.of(L.base));
   atomicMax((long long*)S.key_hi, (long long)G.of((int64_t)((uint64_t)L.base + ext_span)));
+}
+
+// Pattern run (Run::kind 2): rows of cells along a stride s0 in which every
+// cell holds the same set of residue words {t*dg : bit t of pm}: one element
+// per row, its interval spans the row, and the bitmap tier sets the row's
+// sectors from the periodic per-period pattern (lcm(s0, g) / g sectors) word
+// by word instead of one interval per cell and residue cluster.  Returns
+// false (nothing emitted) when the rows would not be monotone.
+constexpr int64_t kPatMinCells = 32;
+__device__ inline int64_t gcd64(int64_t a, int64_t b);
+__device__ __forceinline__ uint32_t pattern_bits(int64_t cell0, uint64_t pm, int64_t dg, int64_t s0, int64_t P,
+                                                 int64_t nph, int64_t g, int shift, int part, int nparts);
+__device__ inline bool emit_pattern(const RunSink& S, const Lat& Lbox, uint64_t cell0, int tag, const Granule& G,
+                                    uint64_t pm, int64_t dg, int64_t s0) {
+  int64_t n0 = Lbox.ex[0];
+  Lat L;  // outer dims (rows), sorted, rows that continue the cell sequence merged into n0
+  L.nd = 0;
+  for (int d = 1; d < Lbox.nd; ++d)
+    if (Lbox.ex[d] > 1) { L.st[L.nd] = Lbox.st[d]; L.ex[L.nd] = Lbox.ex[d]; ++L.nd; }
+  sort_dims(L);
+  while (L.nd > 0 && L.st[0] == (uint64_t)(n0 * s0)) {
+    n0 *= L.ex[0];
+    for (int i = 1; i < L.nd; ++i) { L.st[i - 1] = L.st[i]; L.ex[i - 1] = L.ex[i]; }
+    --L.nd;
+  }
+  if (n0 >= (int64_t(1) << 31)) return false;
+  const int64_t rmin = (int64_t)__ffsll((long long)pm) - 1, rmax = 63 - __clzll((long long)pm);
+  const uint64_t span = (uint64_t)((n0 - 1) * s0 + (rmax - rmin) * dg);
+  unsigned __int128 reach = span;
+  int64_t count = 1;
+  uint64_t ext_span = span;
+  for (int d = 0; d < L.nd; ++d) {
+    if ((unsigned __int128)L.st[d] <= reach) return false;  // rows must be monotone
+    reach += (unsigned __int128)L.st[d] * (uint64_t)(L.ex[d] - 1);
+    if (count > (int64_t(1) << 40) / L.ex[d]) return false;
+    count *= L.ex[d];
+    ext_span += L.st[d] * (uint64_t)(L.ex[d] - 1);
+  }
+  const int slot = atomicAdd(S.n_runs, 1);
+  if (slot >= S.cap) { atomicExch(S.status, GVO_ERR_CAPACITY); return true; }
+  const uint64_t base = cell0 + (uint64_t)(rmin * dg);
+  Run* r = S.runs + slot;
+  r->base = (int64_t)base;
+  r->span = span;
+  r->nd = L.nd;
+  for (int d = 0; d < kMaxDims; ++d) {
+    r->stride[d] = d < L.nd ? (int64_t)L.st[d] : 0;
+    r->ext[d] = d < L.nd ? L.ex[d] : 1;
+  }
+  r->tag = tag;
+  r->kind = 2;
+  r->access = (int32_t)n0;       // cells per row
+  r->pad_ = (int32_t)dg;         // residue unit (bytes)
+  r->run_start = (int64_t)pm;    // residues present, in units of dg
+  r->run_count = s0;             // cell stride (bytes)
+  r->mono = 1;
+  {  // period pattern of rows with this run's phase (cell0 mod g), kept in `pieces`
+    const int64_t gc = gcd64(s0, G.g);
+    const int64_t ph = floormod((int64_t)cell0, G.g);
+    const uint32_t pat = pattern_bits((int64_t)cell0, pm, dg, s0, s0 / gc, G.g / gc, G.g, G.shift, 0, 1);
+    r->pieces = (int64_t)(((uint64_t)ph << 32) | pat);
+  }
+  r->count = count;
+  atomicMin((long long*)S.key_lo, (long long)G.of((int64_t)base));
+  atomicMax((long long*)S.key_hi, (long long)G.of((int64_t)(base + ext_span)));
+  if (S.has_pattern) atomicExch(S.has_pattern, 1);
+  return true;
+}
+
+__device__ inline int64_t gcd64(int64_t a, int64_t b) {  // a, b >= 0
+  while (b) { const int64_t t = a % b; a = b; b = t; }
+  return a;
 }
 
 // Warp-cooperative version: the class's translates P[0..n) (n <= 64, sorted,
@@ -399,7 +473,7 @@ __device__ __forceinline__ int64_t floordiv128(__int128 a, __int128 b, __int128*
 // Returns false (nothing emitted) when the class is not of that shape or
 // the segment plan is not cheaper than cover_warp's.
 __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, const int64_t* P, int n, int tag,
-                               const Granule& G, SegScratch* sc) {
+                               const Granule& G, SegScratch* sc, bool allow_pattern) {
   const int lane = threadIdx.x & 31;
   const int nd = L0.nd;
   if (nd < 1 || nd > kSegDims || n < 2 || n > 64) return false;
@@ -648,6 +722,27 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
       L.st[d] = L0.st[d];
       L.ex[d] = (int64_t)(sc->bp[d][sd[d] + 1] - sc->bp[d][sd[d]]);
       base += L0.st[d] * (uint64_t)(int64_t)sc->bp[d][sd[d]];
+    }
+    // partial cells along a long row: one pattern run instead of one
+    // lattice per residue cluster (unless the clusters fold into the span)
+    if (allow_pattern && L0.span == 0 && L.ex[0] >= kPatMinCells) {
+      const int rf = __ffsll((long long)M) - 1, rl = 63 - __clzll((long long)M);
+      int64_t dg = (int64_t)s0;
+      int ncl = 0;
+      int64_t prev = -1;
+      for (uint64_t m2 = M; m2; m2 &= m2 - 1) {
+        const int q = __ffsll((long long)m2) - 1;
+        dg = gcd64(dg, (int64_t)sc->rs[q]);
+        if (prev < 0 || (int64_t)sc->rs[q] - prev > tol) ++ncl;
+        prev = sc->rs[q];
+      }
+      const bool folds = ncl == 1 && (int64_t)s0 <= (int64_t)(sc->rs[rl] - sc->rs[rf]) + G.g;
+      const int64_t per = (int64_t)s0 / gcd64((int64_t)s0, G.g);  // sectors per pattern period
+      if (!folds && (int64_t)s0 / dg <= 64 && per <= 32) {
+        uint64_t pm = 0;
+        for (uint64_t m2 = M; m2; m2 &= m2 - 1) pm |= 1ull << (sc->rs[__ffsll((long long)m2) - 1] / dg);
+        if (emit_pattern(S, L, base, tag, G, pm, dg, (int64_t)s0)) continue;
+      }
     }
     uint64_t mm = M;
     while (mm) {
@@ -1007,11 +1102,16 @@ __device__ __noinline__ void bm_lattice(uint32_t* bmt, const Run* rrp, int64_t k
                                         int64_t w, int64_t g, int shift) {
   const Run& rr = *rrp;
   const int nd = rr.nd;
-  const uint64_t st0 = nd ? (uint64_t)rr.stride[0] : 0;
-  const int64_t ex0 = nd ? rr.ext[0] : 1;
+  // two-level cursor: dims 0 and 1 stepped incrementally, a full decode only
+  // when dim 1 wraps (segment boxes are often 1-2 cells wide along dim 0)
+  const uint64_t st0 = nd > 0 ? (uint64_t)rr.stride[0] : 0;
+  const int64_t ex0 = nd > 0 ? rr.ext[0] : 1;
+  const uint64_t st1 = nd > 1 ? (uint64_t)rr.stride[1] : 0;
+  const int64_t ex1 = nd > 1 ? rr.ext[1] : 1;
+  const uint64_t back0 = st0 * (uint64_t)(ex0 - 1);
   const uint64_t span = rr.span;
   uint64_t bb = run_base(rr, k);
-  int64_t i0 = nd ? k % ex0 : 0;
+  int64_t i0 = k % ex0, i1 = (k / ex0) % ex1;
   uint32_t* cur_p = nullptr;
   uint32_t cur_m = 0;
   for (int64_t t = 0; t < cnt; ++t) {
@@ -1033,17 +1133,135 @@ __device__ __noinline__ void bm_lattice(uint32_t* bmt, const Run* rrp, int64_t k
       bm_set(bmt, lo, hi);
     }
     if (++i0 < ex0) bb += st0;
-    else { i0 = 0; if (t + 1 < cnt) bb = run_base(rr, k + t + 1); }
+    else {
+      i0 = 0;
+      if (++i1 < ex1) bb += st1 - back0;
+      else { i1 = 0; if (t + 1 < cnt) bb = run_base(rr, k + t + 1); }
+    }
   }
   if (cur_p) atomicOr(cur_p, cur_m);
+}
+
+// Bits of elements [k, k + cnt) of a pattern run (emit_pattern): per row the
+// sectors of cells c < n0 and residues t*dg (bit t of pm) relative to the
+// row's first cell.  The sector set of an unbounded row is periodic with
+// P = s0 / gcd(s0, g) sectors (nph = g / gcd cells); clipped to the row's own
+// first and last sector it is exact: a virtual cell beyond either end can only
+// touch the end sector, which the end cell touches itself.  Each bitmap word
+// is one 32-bit window of the period pattern repeated over 128 bits.
+// Period pattern of a row whose first cell starts at byte cell0: bit j set
+// iff some cell c < nph touches sector G(cell0) + j (mod P).  Depends only on
+// cell0 mod g.
+__device__ __forceinline__ uint32_t pattern_bits(int64_t cell0, uint64_t pm, int64_t dg, int64_t s0, int64_t P,
+                                                 int64_t nph, int64_t g, int shift, int part, int nparts) {
+  // relative to S0 = G(cell0): sector of byte cell0 + y is (ph + y) / g, ph = cell0 mod g
+  const int64_t ph = floormod(cell0, g);
+  const int nt = __popcll(pm);
+  uint32_t pat = 0;
+  for (int64_t p = part; p < nph * nt; p += nparts) {
+    const int64_t c = p / nt;
+    int ti = (int)(p - c * nt);
+    uint64_t m = pm;
+    for (; ti > 0; --ti) m &= m - 1;
+    const int64_t y = ph + c * s0 + (int64_t)(__ffsll((long long)m) - 1) * dg;
+    int64_t j = shift >= 0 ? (y >> shift) : y / g;  // y >= 0
+    while (j >= P) j -= P;
+    pat |= 1u << j;
+  }
+  return pat;
+}
+
+// Thread mode: this thread sets every word of elements [k, k + cnt); the
+// period pattern is rebuilt only when a row's phase (cell0 mod g) changes.
+__device__ __noinline__ void bm_pattern(uint32_t* bmt, const Run* rrp, int64_t k, int64_t cnt, int64_t kb0,
+                                        int64_t w, int64_t g, int shift) {
+  const Run& rr = *rrp;
+  const int64_t dg = rr.pad_, s0 = rr.run_count;
+  const uint64_t pm = (uint64_t)rr.run_start;
+  const int64_t rmin = (int64_t)(__ffsll((long long)pm) - 1) * dg;
+  const int64_t gc = gcd64(s0, g), P = s0 / gc, nph = g / gc;
+  auto G = [&](int64_t x) { return shift >= 0 ? (x >> shift) : floordiv(x, g); };
+  int64_t phase = (int64_t)((uint64_t)rr.pieces >> 32);  // the stored pattern's phase
+  unsigned __int128 pp = (uint32_t)rr.pieces;
+  for (int64_t sh = P; sh < 128; sh += P) pp |= (unsigned __int128)(uint32_t)rr.pieces << sh;
+  for (int64_t e = 0; e < cnt; ++e) {
+    const uint64_t bel = run_base(rr, k + e);
+    const int64_t cell0 = (int64_t)bel - rmin;
+    int64_t lo = G((int64_t)bel) - kb0, hi = G((int64_t)(bel + rr.span)) - kb0;
+    lo = max(lo, (int64_t)0);
+    hi = min(hi, w - 1);
+    if (lo > hi) continue;
+    const int64_t S0 = G(cell0);
+    const int64_t ph = floormod(cell0, g);
+    if (ph != phase) {
+      phase = ph;
+      const uint32_t pat = pattern_bits(cell0, pm, dg, s0, P, nph, g, shift, 0, 1);
+      pp = pat;
+      for (int64_t sh = P; sh < 128; sh += P) pp |= (unsigned __int128)pat << sh;
+    }
+    const int64_t w0 = lo >> 5, w1 = hi >> 5;
+    int64_t off = floormod(kb0 + (w0 << 5) - S0, P);  // pattern phase of the first word's bit 0
+    const int64_t step = 32 % P;
+    for (int64_t ww = w0; ww <= w1; ++ww) {
+      uint32_t v = (uint32_t)(pp >> off);
+      if (ww == w0) v &= ~0u << (lo & 31);
+      if (ww == w1) v &= ~0u >> (31 - (hi & 31));
+      if (v) atomicOr(bmt + ww, v);
+      off += step;
+      if (off >= P) off -= P;
+    }
+  }
+}
+
+// One element (row) of a pattern run by one warp: lanes build the period
+// pattern together and stride over the row's words.
+__device__ __noinline__ void bm_pattern_warp(uint32_t* bmt, const Run* rrp, int64_t k, int64_t kb0, int64_t w,
+                                             int64_t g, int shift) {
+  const Run& rr = *rrp;
+  const int lane = threadIdx.x & 31;
+  const int64_t dg = rr.pad_, s0 = rr.run_count;
+  const uint64_t pm = (uint64_t)rr.run_start;
+  const int64_t rmin = (int64_t)(__ffsll((long long)pm) - 1) * dg;
+  const int64_t gc = gcd64(s0, g), P = s0 / gc, nph = g / gc;
+  auto G = [&](int64_t x) { return shift >= 0 ? (x >> shift) : floordiv(x, g); };
+  const uint64_t bel = run_base(rr, k);
+  const int64_t cell0 = (int64_t)bel - rmin;
+  int64_t lo = G((int64_t)bel) - kb0, hi = G((int64_t)(bel + rr.span)) - kb0;
+  lo = max(lo, (int64_t)0);
+  hi = min(hi, w - 1);
+  if (lo > hi) return;  // warp-uniform
+  const int64_t S0 = G(cell0);
+  const uint32_t pat = floormod(cell0, g) == (int64_t)((uint64_t)rr.pieces >> 32)
+                           ? (uint32_t)rr.pieces
+                           : __reduce_or_sync(0xffffffffu, pattern_bits(cell0, pm, dg, s0, P, nph, g, shift, lane, 32));
+  unsigned __int128 pp = pat;
+  for (int64_t sh = P; sh < 128; sh += P) pp |= (unsigned __int128)pat << sh;
+  const int64_t w0 = lo >> 5, w1 = hi >> 5;
+  int64_t off = floormod(kb0 + ((w0 + lane) << 5) - S0, P);
+  const int64_t step = (32 * 32) % P;
+  for (int64_t ww = w0 + lane; ww <= w1; ww += 32) {
+    uint32_t v = (uint32_t)(pp >> off);
+    if (ww == w0) v &= ~0u << (lo & 31);
+    if (ww == w1) v &= ~0u >> (31 - (hi & 31));
+    if (v) atomicOr(bmt + ww, v);
+    off += step;
+    if (off >= P) off -= P;
+  }
 }
 
 __device__ __noinline__ void bitmap_range(uint32_t* bm, const Run* druns, const int64_t* rcnt, const int64_t* rka, int nr,
                              int64_t N, int64_t a, int64_t b, int64_t kbase, int n_tags, const Granule& Gr,
                              const TplView& T, int abase, const int64_t* fbase, const int32_t bd[3],
                              const int64_t gd[3], int64_t tpb, UnitSh& U, int64_t* wmax, bool nonmono,
-                             uint32_t tag_mask) {
+                             uint32_t tag_mask, int* big_list, int big_cap) {
   const int64_t wp = (b - a + 31) >> 5;
+  // runs whose every interval covers >= kBigWords bitmap words (folded rows,
+  // merged layers) are filled by the whole CTA after the element pass: one
+  // thread per such interval would hold the CTA at the barrier
+  constexpr int64_t kBigWords = 32;
+  const uint64_t big_span = (uint64_t)(kBigWords * 32) * (uint64_t)Gr.g;
+  __shared__ int n_big;
+  if (threadIdx.x == 0) n_big = 0;
   for (int64_t i = threadIdx.x; i < (int64_t)n_tags * wp; i += kNT) bm[i] = 0u;
   __syncthreads();
   // monotone runs: elements rka[r] .. rka[r] + count, contiguous per thread.
@@ -1067,9 +1285,22 @@ __device__ __noinline__ void bitmap_range(uint32_t* bm, const Run* druns, const 
       const int64_t iend = min(e1, rcnt[ri + 1]);
       if (rka[ri] < 0) { i = iend; continue; }
       const Run& rr = druns[ri];
+      if (rr.kind != 1 && rr.span >= big_span) {  // whole-CTA pass below
+        if (rcnt[ri] >= e0) {  // listed once, by the thread owning its first element
+          const int slot = atomicAdd(&n_big, 1);
+          if (slot < big_cap / 2 - 1) big_list[slot] = ri;
+        }
+        i = iend;
+        continue;
+      }
       uint32_t* bmt = bm + (int64_t)__popc(tag_mask & ((1u << rr.tag) - 1u)) * wp;
       int64_t k = rka[ri] + (i - rcnt[ri]);
       const int64_t kend = k + (iend - i);
+      if (rr.kind == 2) {
+        bm_pattern(bmt, &rr, k, kend - k, kbase + a, b - a, Gr.g, Gr.shift);
+        i = iend;
+        continue;
+      }
       if (rr.kind != 0) {
         for (; k < kend; ++k) {
           int64_t lo, hi;
@@ -1095,6 +1326,80 @@ __device__ __noinline__ void bitmap_range(uint32_t* bm, const Run* druns, const 
       lo = max(lo - kbase, a);
       hi = min(hi - kbase, b - 1);
       if (lo <= hi) bm_set(bm + (int64_t)__popc(tag_mask & ((1u << rr.tag) - 1u)) * wp, lo - a, hi - a);
+    }
+  }
+  __syncthreads();
+  // big runs: their (run, element) pairs dealt to warps, lanes over words
+  {
+    const int nb = min(n_big, big_cap / 2 - 1);
+    int* pref = big_list + big_cap / 2;  // exclusive prefix of the listed runs' element counts
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      int carry = 0;
+      for (int q0 = 0; q0 < nb; q0 += 32) {
+        const int q = q0 + lane;
+        const int v = q < nb ? (int)(rcnt[big_list[q] + 1] - rcnt[big_list[q]]) : 0;
+        int inc = v;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += t;
+        }
+        if (q < nb) pref[q] = carry + inc - v;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane == 0) pref[nb] = carry;
+    }
+    __syncthreads();
+    const int total = pref[nb];
+    const int wq = threadIdx.x >> 5, lq = threadIdx.x & 31;
+    for (int f = wq; f < total; f += kNW) {
+      int lo = 0, hi = nb - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (pref[mid] <= f) lo = mid; else hi = mid - 1;
+      }
+      const int r = big_list[lo];
+      const Run& rr = druns[r];
+      uint32_t* pl = bm + (int64_t)__popc(tag_mask & ((1u << rr.tag) - 1u)) * wp;
+      const int64_t kk = rka[r] + (f - pref[lo]);
+      if (rr.kind == 2) {
+        bm_pattern_warp(pl, &rr, kk, kbase + a, b - a, Gr.g, Gr.shift);
+        continue;
+      }
+      const uint64_t bb = run_base(rr, kk);
+      int64_t glo = Gr.of((int64_t)bb) - kbase - a, ghi = Gr.of((int64_t)(bb + rr.span)) - kbase - a;
+      glo = max(glo, (int64_t)0);
+      ghi = min(ghi, b - a - 1);
+      if (glo > ghi) continue;
+      const int64_t w0 = glo >> 5, w1 = ghi >> 5;
+      for (int64_t ww = w0 + lq; ww <= w1; ww += 32) {
+        uint32_t m = ~0u;
+        if (ww == w0) m &= ~0u << (glo & 31);
+        if (ww == w1) m &= ~0u >> (31 - (ghi & 31));
+        if (m == ~0u) pl[ww] = ~0u; else atomicOr(pl + ww, m);
+      }
+    }
+    if (n_big > nb) {  // list overflow: the unlisted big runs, one warp per element
+      for (int r = 0; r < nr; ++r) {
+        const Run& rr = druns[r];
+        if (rka[r] < 0 || rr.kind == 1 || rr.span < big_span) continue;
+        bool listed = false;
+        for (int q = 0; q < nb && !listed; ++q) listed = big_list[q] == r;
+        if (listed) continue;
+        uint32_t* pl = bm + (int64_t)__popc(tag_mask & ((1u << rr.tag) - 1u)) * wp;
+        for (int64_t e = wq; e < rcnt[r + 1] - rcnt[r]; e += kNW) {
+          if (rr.kind == 2) { bm_pattern_warp(pl, &rr, rka[r] + e, kbase + a, b - a, Gr.g, Gr.shift); continue; }
+          const uint64_t bb = run_base(rr, rka[r] + e);
+          int64_t glo = max(Gr.of((int64_t)bb) - kbase, a) - a, ghi = min(Gr.of((int64_t)(bb + rr.span)) - kbase, b - 1) - a;
+          if (glo > ghi) continue;
+          for (int64_t ww = (glo >> 5) + lq; ww <= (ghi >> 5); ww += 32) {
+            uint32_t m = ~0u;
+            if (ww == (glo >> 5)) m &= ~0u << (glo & 31);
+            if (ww == (ghi >> 5)) m &= ~0u >> (31 - (ghi & 31));
+            atomicOr(pl + ww, m);
+          }
+        }
+      }
     }
   }
   __syncthreads();
@@ -1197,6 +1502,7 @@ struct SetsArgs {
   SplitState* split;        // key-range splitting of oversized units (may be null)
   int64_t sm_cap;           // test hook: cap on shared-memory elements (0 = none)
   int32_t seg_off;          // A/B hook: no segment cover
+  int32_t pat_off;          // A/B hook: no pattern runs
   int32_t epoch;            // launch number; queue slots are ready when ready == epoch
 };
 
@@ -1310,7 +1616,7 @@ __device__ bool micro_unit(const SetsArgs& P, int64_t bidx, uint8_t* reg, int64_
         __syncwarp();
         for (int k = lane; k < m; k += 32) wpts[k] = (int64_t)((uint64_t)L0.base + (uint64_t)cp[p0 + k]);
         __syncwarp();
-        if (P.seg_off || !cover_segments(sink, L0, wpts, m, kind, Gr, seg))
+        if (P.seg_off || !cover_segments(sink, L0, wpts, m, kind, Gr, seg, false))
           cover_warp(sink, L0, wpts, m, kind, Gr);
       }
     }
@@ -1622,6 +1928,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       if (threadIdx.x == 0) {
         U.status = GVO_OK;
         U.n_runs = 0;
+        U.has_pattern = 0;
         U.key_lo = INT64_MAX;
         U.key_hi = INT64_MIN;
         U.n_src = 0;
@@ -1742,7 +2049,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         }
       }
       const int64_t tpb = G.tpb;
-      RunSink sink{runs, (int)P.run_cap, &U.n_runs, &U.status, &U.key_lo, &U.key_hi};
+      RunSink sink{runs, (int)P.run_cap, &U.n_runs, &U.status, &U.key_lo, &U.key_hi, &U.has_pattern};
       __syncthreads();
 
       // ---------------- run building
@@ -1810,7 +2117,8 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
             __syncwarp();
             for (int k = lane; k < m; k += 32) wpts[k] = (int64_t)((uint64_t)L0.base + (uint64_t)cp[p0 + k]);
             __syncwarp();
-            const bool segd = !P.seg_off && cover_segments(sink, L0, wpts, m, U.src_tag[s], Gr, seg);
+            const bool segd = !P.seg_off && cover_segments(sink, L0, wpts, m, U.src_tag[s], Gr, seg,
+                                                            !P.pat_off && (U.kind != 0 || P.mode != 0));
             if (!segd) cover_warp(sink, L0, wpts, m, U.src_tag[s], Gr);
             GVO_PH(if (lane == 0) atomicAdd((unsigned long long*)&ph[segd ? 12 : 13], 1ull);)
           }
@@ -1872,7 +2180,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
 
       // too big for shared memory: turn the unit into a split descriptor
       // and continue as its first key range [0, span]
-      if (U.N > sm_elems && SS) {
+      if ((U.N > sm_elems || U.has_pattern) && SS) {
         __shared__ int64_t desc_off;
         if (threadIdx.x == 0) {
           desc_off = -1;
@@ -1897,6 +2205,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
             h->status = GVO_OK;
             h->tag_mask = 0;
             h->slot = slot;
+            h->has_pattern = U.has_pattern;
           }
         }
         __syncthreads();
@@ -1910,7 +2219,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
             dr[r] = rr;
             tm |= 1u << rr.tag;
             int64_t lo = INT64_MIN, hi = INT64_MAX;  // points runs: unknown extent
-            if (rr.kind == 0) {
+            if (rr.kind != 1) {
               uint64_t ext = rr.span;
               for (int d = 0; d < rr.nd; ++d) ext += (uint64_t)rr.stride[d] * (uint64_t)(rr.ext[d] - 1);
               lo = Gr.of(rr.base) - U.key_lo;
@@ -1938,7 +2247,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           range_b = ((U.key_hi - U.key_lo) / U.R + 1) * U.R;
         }
       }
-      if (!in_range && U.N > P.elem_cap) {  // no descriptor slot free and too big for the slab
+      if (!in_range && (U.N > P.elem_cap || U.has_pattern)) {  // no descriptor slot free (pattern runs need ranges)
         if (threadIdx.x == 0) {
           if (P.mode == 0) {
             int64_t* row = P.counts + c * P.counts_stride;
@@ -1998,6 +2307,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       for (int q = 0; q < U.n_sub; ++q)
         bm_r_ok = bm_r_ok && U.sub_r[q] >= 1 && U.sub_r[q] <= 32 && (32 % U.sub_r[q]) == 0;
       const int64_t bm_words = sm_elems * 4;  // ebuf holds 2*sm_elems 8-byte elements
+      const bool has_pat = *reinterpret_cast<volatile const int32_t*>(&hdr->has_pattern) != 0;
       for (;;) {
         // count in-range elements per run (monotone runs: closed form)
         if (threadIdx.x == 0) s_nonmono = 0;
@@ -2010,7 +2320,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
             continue;
           }
           const Run& rr = druns[r];
-          if (rr.kind == 0 && rr.mono) {
+          if (rr.kind != 1 && rr.mono) {
             const int64_t ka = first >= a ? 0 : mono_first(rr, Gr, kbase, a, true);
             const int64_t kb = last < b ? rr.count : mono_first(rr, Gr, kbase, b, false);
             rka[r] = ka;
@@ -2054,12 +2364,14 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           const int64_t wp = (b - a + 31) >> 5;
           const bool bm_fit = bm_r_ok && (int64_t)n_tags * wp <= bm_words;
           const bool bm_cheaper = acc * 96 > (int64_t)n_tags * wp * 2 + wp * 3 * (int64_t)U.n_sub;
-          s_bm = bm_fit && (acc > sm_elems || bm_cheaper) ? 1 : 0;
-          if (!s_bm && acc > sm_elems && b - a > R) {
+          // pattern runs exist only as bitmaps: such units always take that tier
+          s_bm = bm_fit && (acc > sm_elems || bm_cheaper || has_pat) ? 1 : 0;
+          if (!s_bm && (acc > sm_elems || has_pat) && b - a > R) {
             // split into pieces sized for the tier the density favours (one
             // level instead of repeated halving); piece 0 is processed here
             const double dens = (double)acc / (double)(b - a);
-            const bool bm_pref = bm_r_ok && n_tags > 0 && dens * 96.0 * 32.0 > 2.0 * n_tags + 3.0 * U.n_sub;
+            const bool bm_pref = bm_r_ok && n_tags > 0 &&
+                                 (has_pat || dens * 96.0 * 32.0 > 2.0 * n_tags + 3.0 * U.n_sub);
             int64_t width = bm_pref ? (bm_words / n_tags) * 32
                                     : (int64_t)((double)(b - a) * 0.8 * (double)sm_elems / (double)acc);
             width = max(R, (width / R) * R);
@@ -2108,11 +2420,12 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       GVO_PH(if (threadIdx.x == 0) { ph[5] += t_r1 - t_r0; ph[8] += 1; ph[9] += s_bm; ph[10] += N; ph[11] += nr; })
       if (s_bm) {
         bitmap_range(reinterpret_cast<uint32_t*>(ebuf), druns, rcnt, rka, nr, N, a, b, kbase, n_tags, Gr, P.T, abase,
-                     fbase, bd, gd, tpb, U, wmax, s_nonmono != 0, tag_mask);
+                     fbase, bd, gd, tpb, U, wmax, s_nonmono != 0, tag_mask, reinterpret_cast<int*>(hist),
+                     kNW * 256);
         if (threadIdx.x < U.n_sub) atomicAdd(&hdr->acc[threadIdx.x], (unsigned long long)U.sub_val[threadIdx.x]);
         GVO_PH(if (threadIdx.x == 0) ph[6] += clock64() - t_r1;)
-      } else if (N > P.elem_cap) {
-        if (threadIdx.x == 0) atomicExch(&hdr->status, GVO_ERR_CAPACITY);
+      } else if (N > P.elem_cap || has_pat) {
+        if (threadIdx.x == 0) atomicExch(&hdr->status, has_pat ? GVO_ERR_UNSUPPORTED : GVO_ERR_CAPACITY);
       } else {
         uint64_t* A0 = N <= sm_elems ? ebuf : gbuf;
         uint64_t* B0 = N <= sm_elems ? ebuf + sm_elems : gbuf + P.elem_cap;
@@ -2391,6 +2704,7 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st) {
   P.split = L.split;
   P.sm_cap = L.sm_cap;
   P.seg_off = L.seg_off;
+  P.pat_off = L.pat_off;
   P.epoch = L.epoch;  // never 0 (the zeroed initial state), unique per launch
   if (P.n_items + P.n_warp_items <= 0) return;
   cudaMemsetAsync(P.work, 0, sizeof(unsigned long long), st);
