@@ -221,14 +221,13 @@ def test_split_ranges_forced_small_capacity():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-def _interleaved_kernel(rng):
+def _interleaved_kernel(rng, W=16, H=8, D=6):
     """A field with Q interleaved 8-byte components per cell (zyxf layout), read
     by pull loads q <- cell + c_q (c_q random neighbour offsets) and written in
     place: the translate classes whose residues tile a cell, which the set
     engine covers by segment boxes (k_sets.cu cover_segments)."""
     Q = int(rng.choice([3, 5, 9, 15, 27]))
-    W, H, D = 16, 8, 6
-    block = [(4, 2, 1), (8, 1, 2), (2, 4, 3), (16, 2, 1), (1, 8, 2), (4, 4, 2)][rng.integers(0, 6)]
+    block = [(4, 2, 1), (8, 1, 2), (2, 4, 2), (16, 2, 1), (1, 4, 2), (4, 4, 2)][rng.integers(0, 6)]
     grid = (W // block[0], H // block[1], D // block[2])
     fields = (gvo.Field("src", 8, (W * H * D * Q,), alignment=int(rng.choice([0, 8, 24]))),
               gvo.Field("dst", 8, (W * H * D * Q,), alignment=0))
@@ -271,3 +270,19 @@ def test_interleaved_evaluations_vs_oracle():
         ev = ora.evaluate_kernel(k, m, override=ov or None)
         assert p.glups == ev["glups"] and p.limiter == ev["limiter"], i
         assert p.volumes.dram_load.v_down == ev["volumes"]["dram_load"]["down"], i
+
+
+def test_interleaved_long_rows_vs_oracle():
+    """Rows of 64 cells: boundary layers with partial component sets become
+    pattern runs (k_sets.cu emit_pattern / bm_pattern)."""
+    rng = np.random.default_rng(1143)
+    for i in range(40):
+        k = _interleaved_kernel(rng, W=64, H=4, D=4)
+        nb = k.launch.total_blocks
+        cnt = int(rng.integers(max(1, nb // 4), nb + 1))
+        start = int(rng.integers(0, nb - cnt + 1))
+        g = int(rng.choice([8, 24, 32, 128]))
+        grp = CollaborativeGroup(k.launch, np.arange(start, start + cnt, dtype=np.int64), "L2")
+        r = gvo.grid_iteration(k, grp, g)
+        got = {(f, kd): (c.unique_count, c.total_count) for (f, kd), c in r.per_field.items()}
+        assert got == ora.footprint(k, grp.block_linear, g), (i, k.launch, len(k.accesses) // 2, g)
