@@ -130,14 +130,17 @@ __global__ void __launch_bounds__(1024) k_rank_small(const double* rec, const gv
             ((uint64_t)(c.block[2] & 0xfffff) << 2) | (uint64_t)(c.fold_rank & 3);
   }
   __syncthreads();
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+  // one warp per element: lanes count a strided share of the others, then reduce
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t i = wid; i < n; i += nw) {
     const uint64_t a1 = s1[i], a2 = s2[i];
-    int64_t r = 0;
-    for (int64_t j = 0; j < n; ++j) {
+    int r = 0;
+    for (int64_t j = lane; j < n; j += 32) {
       const uint64_t b1 = s1[j], b2 = s2[j];
       r += (b1 < a1) || (b1 == a1 && (b2 < a2 || (b2 == a2 && j < i)));
     }
-    order[r] = i;
+    r = __reduce_add_sync(0xffffffffu, r);
+    if (lane == 0) order[r] = i;
   }
 }
 
