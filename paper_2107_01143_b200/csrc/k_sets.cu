@@ -451,7 +451,10 @@ constexpr int kSegDims = 4;
 constexpr int kSegBp = 66;          // breakpoints per dimension (<= 65 used: 64 segments)
 constexpr int kSegMaxBoxes = 4096;
 constexpr int kSegScratch = 2688;   // bytes of per-warp scratch
-constexpr int64_t kSegRunWeight = 100;  // element-equivalents of one extra run (measured: ~1.2k cycles to build a run, ~12 per sorted element)
+#ifndef GVO_SEG_RUN_WEIGHT
+#define GVO_SEG_RUN_WEIGHT 48
+#endif
+constexpr int64_t kSegRunWeight = GVO_SEG_RUN_WEIGHT;  // element-equivalents of one extra run (100 measured worse on C3)
 struct SegScratch {
   int32_t kv[kSegDims][64];  // offsets per dimension, by translate
   int32_t bp[kSegDims][kSegBp];
@@ -483,6 +486,19 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
     if (L0.ex[d] >= (int64_t(1) << 29) || L0.st[d] >= (uint64_t(1) << 62)) return false;
   const int64_t tol = (int64_t)L0.span + G.g;
   if ((int64_t)n * tol < (int64_t)s0) return false;  // n residues cannot tile a cell
+  {  // cheap screen: distinct residues mod s0 (one match per lane) must be able to tile it
+    int distinct = 0;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      const bool v = i < n;
+      const int64_t r = v ? floormod((int64_t)((uint64_t)P[i] - (uint64_t)L0.base), (int64_t)s0) : -1;
+      const unsigned act = __ballot_sync(0xffffffffu, v);
+      unsigned peers = 0;
+      if (v) peers = __match_any_sync(act, (unsigned long long)r);
+      distinct += __popc(__ballot_sync(0xffffffffu, v && (__ffs(peers) - 1) == lane));
+    }
+    if ((int64_t)distinct * tol < (int64_t)s0) return false;
+  }
   // 1. offsets: round to nearest along the outer dims, floor along dim 0
   bool ok = true;
   for (int i = lane; i < n; i += 32) {
