@@ -452,9 +452,9 @@ constexpr int kSegBp = 66;          // breakpoints per dimension (<= 65 used: 64
 constexpr int kSegMaxBoxes = 4096;
 constexpr int kSegScratch = 2688;   // bytes of per-warp scratch
 #ifndef GVO_SEG_RUN_WEIGHT
-#define GVO_SEG_RUN_WEIGHT 48
+#define GVO_SEG_RUN_WEIGHT 16
 #endif
-constexpr int64_t kSegRunWeight = GVO_SEG_RUN_WEIGHT;  // element-equivalents of one extra run (100 measured worse on C3)
+constexpr int64_t kSegRunWeight = GVO_SEG_RUN_WEIGHT;  // element-equivalents of one extra run (A/B on C3: 16 > 32 > 48 > 100)
 struct SegScratch {
   int32_t kv[kSegDims][64];  // offsets per dimension, by translate
   int32_t bp[kSegDims][kSegBp];
