@@ -146,6 +146,13 @@ static __device__ __noinline__ void warp_item(const WarpArgs& W, int64_t item, u
     uint32_t skip_field = 0;  // fields whose sample is a translate of an earlier one
     if (mode == 0 && !is_l1)
       for (int f = 0; f < kMaxFields; ++f) skip_field |= (geos[c].dup_of[f][j] >= 0 ? 1u : 0u) << f;
+    // every field of this sample is a translate of an earlier sample: k_finish
+    // copies all its counts, nothing to evaluate (uniform across the CTA)
+    {
+      const int nf = T.n_fields[tpl];
+      const uint32_t all = nf >= 32 ? ~0u : ((1u << nf) - 1u);
+      if (mode == 0 && !is_l1 && nf > 0 && (skip_field & all) == all) return;
+    }
     __syncthreads();
     // group of each access: first access of the same field, kind and
     // coefficients whose constant (block terms included) has the same residue
