@@ -2105,6 +2105,8 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         }
       }
       // (b) lattices: one WARP per (source, box, coefficient class)
+      GVO_PH(__syncthreads(); if (threadIdx.x == 0) ph[14] += clock64() - t_start;)
+      GVO_PH(const long long t_lat = clock64();)
       {
         const CTab ct{const_cast<int64_t*>(P.ctabs) + c * ctab_stride(P.T.max_acc), P.T.max_acc};
         const int slot0 = U.field * 2;
@@ -2115,8 +2117,40 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         int64_t* wpts = cpts + wid * kClassPts;
         // hist .. rka are free while runs are built
         SegScratch* seg = reinterpret_cast<SegScratch*>(micro_region + wid * kSegScratch);
-        for (int task = wid; task < U.n_src * 5 * ncl; task += kNW) {
-          const int s = task / (5 * ncl), rem = task % (5 * ncl), bi = rem / ncl, ci = rem % ncl;
+        // the real (source, box, class) tasks, compacted so that warps share
+        // them evenly (empty store sources and absent boxes are skipped);
+        // the element buffer is free while runs are built
+        __shared__ int n_tasks_sh;
+        int* tlist = reinterpret_cast<int*>(ebuf);
+        const int tcap = (int)min((int64_t)1 << 20, sm_elems * 4);
+        if (threadIdx.x == 0) {
+          int nt = 0;
+          for (int s2 = 0; s2 < U.n_src && nt >= 0; ++s2) {
+            const int slot = slot0 + U.src_kind[s2];
+            const int nc = (int)(ct.slot_first()[slot + 1] - ct.slot_first()[slot]);
+            if (nc <= 0) continue;
+            Box bx[5];
+            const int nb = run_boxes(U.src_start[s2], U.src_count[s2], gd, bx);
+            for (int bi = 0; bi < nb && nt >= 0; ++bi)
+              for (int ci = 0; ci < nc; ++ci) {
+                if (nt >= tcap) { nt = -1; break; }
+                tlist[nt++] = (s2 << 20) | (bi << 16) | ci;  // n_src <= 64, boxes < 8, classes < 65536
+              }
+          }
+          n_tasks_sh = nt;
+        }
+        __syncthreads();
+        const int n_tasks = n_tasks_sh;
+        const bool listed = n_tasks >= 0 && ncl < 65536;
+        const int n_iter = listed ? n_tasks : U.n_src * 5 * ncl;
+        for (int task = wid; task < n_iter; task += kNW) {
+          int s, bi, ci;
+          if (listed) {
+            const int t = tlist[task];
+            s = t >> 20; bi = (t >> 16) & 15; ci = t & 0xffff;
+          } else {
+            s = task / (5 * ncl); const int rem = task % (5 * ncl); bi = rem / ncl; ci = rem % ncl;
+          }
           const int slot = slot0 + U.src_kind[s];
           const int64_t cl0 = ct.slot_first()[slot];
           if (ci >= ct.slot_first()[slot + 1] - cl0) continue;
@@ -2141,6 +2175,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         }
       }
       __syncthreads();
+      GVO_PH(if (threadIdx.x == 0) ph[15] += clock64() - t_lat;)
 
     if (threadIdx.x == 0) { t_runs_sh = clock64(); GVO_PH(ph[3] += t_runs_sh - t_start;) }
     // ---------------- offsets of runs, element count
@@ -2168,8 +2203,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       if (threadIdx.x == 0) {
         const int64_t acc = roff[nr];
         U.N = acc;
-        GVO_PH(ph[14] += acc;)
-        GVO_PH(ph[15] += nr;)
+
         const int64_t base = floordiv(U.key_lo, U.R) * U.R;
         U.key_lo = base;
         if (U.status == GVO_OK) {

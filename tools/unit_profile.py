@@ -72,7 +72,7 @@ names = ["fetch-wait", "warp-items", "micro", "unit-runs", "unit-sort/sweep", "r
          "range-emit/sort/sweep"]
 tot = ph[:, :8].sum(0) / 1e6
 print("CTAs", len(ph), "phase Gcycles (sum over CTAs):", {n: round(v / 1e3, 3) for n, v in zip(names, tot)})
-print("ranges", int(ph[:, 8].sum()), "bitmap", int(ph[:, 9].sum()), "sum N", int(ph[:, 10].sum()), "sum nr", int(ph[:, 11].sum()), "seg ok", int(ph[:, 12].sum()), "seg no", int(ph[:, 13].sum()), "unit N", int(ph[:, 14].sum()), "unit runs", int(ph[:, 15].sum()))
+print("ranges", int(ph[:, 8].sum()), "bitmap", int(ph[:, 9].sum()), "sum N", int(ph[:, 10].sum()), "sum nr", int(ph[:, 11].sum()), "seg ok", int(ph[:, 12].sum()), "seg no", int(ph[:, 13].sum()), "runs: pre-lattice Gcyc", round(ph[:, 14].sum() / 1e9, 3), "lattice Gcyc", round(ph[:, 15].sum() / 1e9, 3))
 fw = ph[:, 0] / 1e3
 busy = ph[:, 1:8].sum(1) / 1e3
 print("per-CTA fetch-wait kcycles p10/p50/p90/max", np.percentile(fw, [10, 50, 90, 100]).round(0),
