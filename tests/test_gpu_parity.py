@@ -286,3 +286,34 @@ def test_interleaved_long_rows_vs_oracle():
         r = gvo.grid_iteration(k, grp, g)
         got = {(f, kd): (c.unique_count, c.total_count) for (f, kd), c in r.per_field.items()}
         assert got == ora.footprint(k, grp.block_linear, g), (i, k.launch, len(k.accesses) // 2, g)
+
+
+def test_rank_sweep_sharded_matches_rank_sweep():
+    """The multi-GPU sweep API (one all-gather + device ranking) on one rank
+    with a real NCCL process group, and without one: same order and records
+    as rank_sweep."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    m = gvo.b200_preset()
+    fam = gvo.KernelFamily("stencil", (64, 64, 64), radius=3)
+    cfgs = list(gvo.enumerate_sweep(128, foldings=("none", "2y", "2z"))) + list(gvo.enumerate_sweep(256))
+    ref = gvo.rank_sweep(fam, cfgs, m, skip_invalid=True)
+    kept, order, rec = gvo.rank_sweep_sharded(fam, cfgs, m, skip_invalid=True)
+    assert [kept[i].key for i in order] == [r.config.key for r in ref]
+    np.testing.assert_array_equal(rec[order], np.asarray(ref.records)[ref.order])
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        kept2, order2, rec2 = gvo.rank_sweep_sharded(fam, cfgs, m, skip_invalid=True)
+    finally:
+        dist.destroy_process_group()
+    assert [k.key for k in kept2] == [k.key for k in kept]
+    np.testing.assert_array_equal(order2, order)
+    np.testing.assert_array_equal(rec2, rec)
