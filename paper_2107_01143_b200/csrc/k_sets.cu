@@ -448,7 +448,7 @@ __device__ GVO_NOINL void cover_warp(const RunSink& S, const Lat& L0, const int6
 // and rows collapse into intervals.  Exact: the segment boxes partition the
 // union of the B_p (any decomposition of the offsets is valid).
 constexpr int kSegDims = 4;
-constexpr int kSegBp = 66;          // breakpoints per dimension (<= 65 used: 64 segments)
+constexpr int kSegBpAll = 264;      // breakpoints over all dimensions (flat)
 constexpr int kSegMaxBoxes = 4096;
 constexpr int kSegScratch = 2688;   // bytes of per-warp scratch
 #ifndef GVO_SEG_RUN_WEIGHT
@@ -457,7 +457,8 @@ constexpr int kSegScratch = 2688;   // bytes of per-warp scratch
 constexpr int64_t kSegRunWeight = GVO_SEG_RUN_WEIGHT;  // element-equivalents of one extra run (A/B on C3: 16 > 32 > 48 > 100)
 struct SegScratch {
   int32_t kv[kSegDims][64];  // offsets per dimension, by translate
-  int32_t bp[kSegDims][kSegBp];
+  int32_t bpf[kSegBpAll];    // breakpoints, dimension d at boff[d]
+  int32_t boff[kSegDims];
   int32_t rs[64];            // residues, sorted
   int32_t tmp[64];
   int32_t nb[kSegDims];
@@ -623,18 +624,21 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
       both |= (uint64_t)bb << (32 * t);
     }
     const int nmerged = 2 * m - __popcll(both);
-    if (nmerged > kSegBp - 1) return false;
+    const int b0 = d == 0 ? 0 : sc->boff[d - 1] + sc->nb[d - 1];
+    if (b0 + nmerged > kSegBpAll) return false;
+    if (lane == 0) sc->boff[d] = b0;
+    __syncwarp();
     for (int t = 0; t < 2; ++t) {
       const int i = lane + 32 * t;
       if (i >= m) continue;
       const int32_t x = sc->tmp[i];
       const uint64_t below_i = i ? (~0ull >> (64 - i)) : 0ull;
-      sc->bp[d][i + lbD(x - ex) - __popcll(both & below_i)] = x;
+      sc->bpf[sc->boff[d] + (i + lbD(x - ex) - __popcll(both & below_i))] = x;
       const int32_t y = x + ex;
       const int j = lbD(y);
       if (!(j < m && sc->tmp[j] == y)) {
         const uint64_t below_j = j ? (j >= 64 ? ~0ull : (~0ull >> (64 - j))) : 0ull;
-        sc->bp[d][j + i - __popcll(both & below_j)] = y;
+        sc->bpf[sc->boff[d] + (j + i - __popcll(both & below_j))] = y;
       }
     }
     if (lane == 0) sc->nb[d] = nmerged;
@@ -644,6 +648,8 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
   }
   // 4. per-dimension segment masks over sorted positions (lane holds
   // segments lane and lane + 32)
+  bool fly = false;  // a dimension with > 64 segments: masks computed per box
+  for (int d = 0; d < nd; ++d) fly |= sc->nb[d] - 1 > 64;
   uint64_t segm[kSegDims][2];
 #pragma unroll
   for (int d = 0; d < kSegDims; ++d) {
@@ -651,8 +657,8 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
     for (int h = 0; h < 2; ++h) {
       segm[d][h] = 0;
       const int sg = lane + 32 * h;
-      if (d < nd && sg < sc->nb[d] - 1) {
-        const int32_t lo = sc->bp[d][sg], hi = sc->bp[d][sg + 1];
+      if (!fly && d < nd && sg < sc->nb[d] - 1) {
+        const int32_t lo = sc->bpf[sc->boff[d] + (sg)], hi = sc->bpf[sc->boff[d] + (sg + 1)];
         const int32_t ex = (int32_t)L0.ex[d];
         for (int r = 0; r < n; ++r) {
           const int32_t k = sc->kv[d][sc->ord[r]];
@@ -677,16 +683,28 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
       }
     }
     uint64_t M = ~0ull;
+    if (!fly) {
 #pragma unroll
-    for (int d = 0; d < kSegDims; ++d) {
-      const uint64_t v0 = __shfl_sync(0xffffffffu, segm[d][0], sd[d] & 31);
-      const uint64_t v1 = __shfl_sync(0xffffffffu, segm[d][1], sd[d] & 31);
-      if (d < nd) M &= sd[d] >= 32 ? v1 : v0;
+      for (int d = 0; d < kSegDims; ++d) {
+        const uint64_t v0 = __shfl_sync(0xffffffffu, segm[d][0], sd[d] & 31);
+        const uint64_t v1 = __shfl_sync(0xffffffffu, segm[d][1], sd[d] & 31);
+        if (d < nd) M &= sd[d] >= 32 ? v1 : v0;
+      }
+    } else if (b < nbox) {
+      M = 0;
+      for (int r2 = 0; r2 < n; ++r2) {
+        bool in = true;
+        for (int d = 0; d < nd && in; ++d) {
+          const int32_t k = sc->kv[d][sc->ord[r2]];
+          in = k <= sc->bpf[sc->boff[d] + sd[d]] && sc->bpf[sc->boff[d] + sd[d] + 1] <= k + (int32_t)L0.ex[d];
+        }
+        if (in) M |= 1ull << r2;
+      }
     }
     if (b >= nbox || !M) continue;
     double vol = 1.0;
-    for (int d = 0; d < nd; ++d) vol *= (double)(sc->bp[d][sd[d] + 1] - sc->bp[d][sd[d]]);
-    const double len0 = (double)(sc->bp[0][sd[0] + 1] - sc->bp[0][sd[0]]);
+    for (int d = 0; d < nd; ++d) vol *= (double)(sc->bpf[sc->boff[d] + sd[d] + 1] - sc->bpf[sc->boff[d] + sd[d]]);
+    const double len0 = (double)(sc->bpf[sc->boff[0] + sd[0] + 1] - sc->bpf[sc->boff[0] + sd[0]]);
     uint64_t mm = M;
     while (mm) {
       const int r0 = __ffsll((long long)mm) - 1;
@@ -724,11 +742,23 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
       }
     }
     uint64_t M = ~0ull;
+    if (!fly) {
 #pragma unroll
-    for (int d = 0; d < kSegDims; ++d) {
-      const uint64_t v0 = __shfl_sync(0xffffffffu, segm[d][0], sd[d] & 31);
-      const uint64_t v1 = __shfl_sync(0xffffffffu, segm[d][1], sd[d] & 31);
-      if (d < nd) M &= sd[d] >= 32 ? v1 : v0;
+      for (int d = 0; d < kSegDims; ++d) {
+        const uint64_t v0 = __shfl_sync(0xffffffffu, segm[d][0], sd[d] & 31);
+        const uint64_t v1 = __shfl_sync(0xffffffffu, segm[d][1], sd[d] & 31);
+        if (d < nd) M &= sd[d] >= 32 ? v1 : v0;
+      }
+    } else if (b < nbox) {
+      M = 0;
+      for (int r2 = 0; r2 < n; ++r2) {
+        bool in = true;
+        for (int d = 0; d < nd && in; ++d) {
+          const int32_t k = sc->kv[d][sc->ord[r2]];
+          in = k <= sc->bpf[sc->boff[d] + sd[d]] && sc->bpf[sc->boff[d] + sd[d] + 1] <= k + (int32_t)L0.ex[d];
+        }
+        if (in) M |= 1ull << r2;
+      }
     }
     if (b >= nbox || !M) continue;
     Lat L;
@@ -736,8 +766,8 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
     uint64_t base = (uint64_t)L0.base;
     for (int d = 0; d < nd; ++d) {
       L.st[d] = L0.st[d];
-      L.ex[d] = (int64_t)(sc->bp[d][sd[d] + 1] - sc->bp[d][sd[d]]);
-      base += L0.st[d] * (uint64_t)(int64_t)sc->bp[d][sd[d]];
+      L.ex[d] = (int64_t)(sc->bpf[sc->boff[d] + sd[d] + 1] - sc->bpf[sc->boff[d] + sd[d]]);
+      base += L0.st[d] * (uint64_t)(int64_t)sc->bpf[sc->boff[d] + sd[d]];
     }
     // partial cells along a long row: one pattern run instead of one
     // lattice per residue cluster (unless the clusters fold into the span)
@@ -2347,7 +2377,9 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       int64_t* rcnt = nr <= kSmemRuns ? roff_sh : roff_gl;
       int64_t* rka = nr <= kSmemRuns ? rka_sh : rka_gl;
       __shared__ int64_t s_N;
-      __shared__ int s_split, s_bm, s_nonmono;
+      __shared__ int s_split, s_bm, s_nonmono, s_m;
+      __shared__ int64_t s_width;
+      __shared__ unsigned long long s_pmask;
       int64_t a = range_a, b = range_b;
       const long long t_r0 = clock64();
       // tags present in the runs (the bitmap keeps one plane per present
@@ -2416,7 +2448,8 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           const bool bm_cheaper = acc * 96 > (int64_t)n_tags * wp * 2 + wp * 3 * (int64_t)U.n_sub;
           // pattern runs exist only as bitmaps: such units always take that tier
           s_bm = bm_fit && (acc > sm_elems || bm_cheaper || has_pat) ? 1 : 0;
-          if (!s_bm && (acc > sm_elems || has_pat) && b - a > R) {
+          s_m = 1;
+          if (!s_bm && acc > 0 && (acc > sm_elems || has_pat) && b - a > R) {
             // split into pieces sized for the tier the density favours (one
             // level instead of repeated halving); piece 0 is processed here
             const double dens = (double)acc / (double)(b - a);
@@ -2431,18 +2464,41 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
               width = (((b - a) / 64) / R + 1) * R;
               m = (b - a + width - 1) / width;
             }
-            if (m > 1) {
-              atomicAdd(&hdr->outstanding, (int)(m - 1));
-              atomicAdd(&SS->pending, (unsigned long long)(m - 1));
-              const unsigned long long slot0 = atomicAdd(&SS->qtail, (unsigned long long)(m - 1));
+            s_m = (int)m;
+            s_width = width;
+            s_pmask = 0ull;
+          }
+        }
+        __syncthreads();
+        if (s_m > 1) {
+          // pieces no run reaches are not queued (sparse units: rows far apart)
+          const int64_t width = s_width;
+          const int m = s_m;
+          for (int r = threadIdx.x; r < nr; r += kNT) {
+            const int64_t f0 = max(dlim[2 * r], a), f1 = min(dlim[2 * r + 1], b - 1);
+            if (f0 > f1) continue;
+            const int p0 = (int)((f0 - a) / width), p1 = (int)min((int64_t)m - 1, (f1 - a) / width);
+            const uint64_t bits = (p1 - p0 >= 63 ? ~0ull : ((2ull << (p1 - p0)) - 1ull)) << p0;
+            atomicOr(&s_pmask, (unsigned long long)bits);
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            const uint64_t pm = s_pmask & ~1ull;  // piece 0 stays here
+            const int nq = __popcll(pm);
+            if (nq > 0) {
+              atomicAdd(&hdr->outstanding, nq);
+              atomicAdd(&SS->pending, (unsigned long long)nq);
+              const unsigned long long slot0 = atomicAdd(&SS->qtail, (unsigned long long)nq);
               const int64_t desc = (int64_t)(reinterpret_cast<uint8_t*>(hdr) - SS->arena);
-              for (int64_t t = 1; t < m; ++t) {
-                const unsigned long long slot = slot0 + (unsigned long long)(t - 1);
+              int qi = 0;
+              for (uint64_t mm = pm; mm; mm &= mm - 1, ++qi) {
+                const int t = __ffsll((long long)mm) - 1;
+                const unsigned long long slot = slot0 + (unsigned long long)qi;
                 if ((int64_t)slot < SS->q_cap) {
                   RangeItem it;
                   it.desc = desc;
-                  it.a = a + t * width;
-                  it.b = min(b, a + (t + 1) * width);
+                  it.a = a + (int64_t)t * width;
+                  it.b = min(b, a + ((int64_t)t + 1) * width);
                   it.ready = 0;
                   it.pad = 0;
                   SS->queue[slot] = it;
@@ -2454,10 +2510,12 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
                   atomicAdd(&SS->pending, ~0ull);
                 }
               }
-              s_split = 1;
-              b = a + width;
             }
+            s_split = 1;
+            cur_range.a = a;
+            cur_range.b = a + width;
           }
+        } else if (threadIdx.x == 0) {
           cur_range.a = a;
           cur_range.b = b;
         }
@@ -2468,7 +2526,9 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       const int64_t N = s_N;
       const long long t_r1 = clock64();
       GVO_PH(if (threadIdx.x == 0) { ph[5] += t_r1 - t_r0; ph[8] += 1; ph[9] += s_bm; ph[10] += N; ph[11] += nr; })
-      if (s_bm) {
+      if (N == 0) {
+        // empty key range (sparse units: rows far apart): every measure adds 0
+      } else if (s_bm) {
         bitmap_range(reinterpret_cast<uint32_t*>(ebuf), druns, rcnt, rka, nr, N, a, b, kbase, n_tags, Gr, P.T, abase,
                      fbase, bd, gd, tpb, U, wmax, s_nonmono != 0, tag_mask, reinterpret_cast<int*>(hist),
                      kNW * 256);
