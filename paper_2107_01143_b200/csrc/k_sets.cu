@@ -2380,6 +2380,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       __shared__ int s_split, s_bm, s_nonmono, s_m;
       __shared__ int64_t s_width;
       __shared__ unsigned long long s_pmask;
+      __shared__ uint32_t s_rtags;
       int64_t a = range_a, b = range_b;
       const long long t_r0 = clock64();
       // tags present in the runs (the bitmap keeps one plane per present
@@ -2392,8 +2393,9 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       const bool has_pat = *reinterpret_cast<volatile const int32_t*>(&hdr->has_pattern) != 0;
       for (;;) {
         // count in-range elements per run (monotone runs: closed form)
-        if (threadIdx.x == 0) s_nonmono = 0;
+        if (threadIdx.x == 0) { s_nonmono = 0; s_rtags = 0u; }
         __syncthreads();
+        uint32_t my_tags = 0;  // tags of the runs with elements in [a, b)
         for (int r = threadIdx.x; r < nr; r += kNT) {
           const int64_t first = dlim[2 * r], last = dlim[2 * r + 1];
           if (last < a || first >= b) {  // whole run outside [a, b)
@@ -2407,12 +2409,16 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
             const int64_t kb = last < b ? rr.count : mono_first(rr, Gr, kbase, b, false);
             rka[r] = ka;
             rcnt[r] = kb > ka ? kb - ka : 0;
+            if (kb > ka) my_tags |= 1u << rr.tag;
           } else {
             rka[r] = -1;
             rcnt[r] = 0;
             s_nonmono = 1;
+            my_tags |= 1u << rr.tag;  // conservatively present
           }
         }
+        my_tags = __reduce_or_sync(0xffffffffu, my_tags);
+        if ((threadIdx.x & 31) == 0 && my_tags) atomicOr(&s_rtags, my_tags);
         __syncthreads();
         // non-monotone runs: scan all their elements (rare)
         for (int r = 0; r < (s_nonmono ? nr : 0); ++r) {
@@ -2444,7 +2450,9 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           // element buffer, when the range is narrow enough and dense enough
           // that setting bits beats emitting + radix sorting intervals
           const int64_t wp = (b - a + 31) >> 5;
-          const bool bm_fit = bm_r_ok && (int64_t)n_tags * wp <= bm_words;
+          // bitmap planes only for the tags present in this range
+          const int n_tags_r = max(1, __popc(s_rtags & tag_mask));
+          const bool bm_fit = bm_r_ok && (int64_t)n_tags_r * wp <= bm_words;
           const bool bm_cheaper = acc * 96 > (int64_t)n_tags * wp * 2 + wp * 3 * (int64_t)U.n_sub;
           // pattern runs exist only as bitmaps: such units always take that tier
           s_bm = bm_fit && (acc > sm_elems || bm_cheaper || has_pat) ? 1 : 0;
@@ -2455,9 +2463,13 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
             const double dens = (double)acc / (double)(b - a);
             const bool bm_pref = bm_r_ok && n_tags > 0 &&
                                  (has_pat || dens * 96.0 * 32.0 > 2.0 * n_tags + 3.0 * U.n_sub);
-            int64_t width = bm_pref ? (bm_words / n_tags) * 32
+            // pieces of a wave unit mostly hold one wave's tags
+            int est_tags = max(1, U.kind == 1 && hdr->n_uw > 1 ? (n_tags_r + hdr->n_uw - 1) / hdr->n_uw : n_tags_r);
+            if ((bm_words / est_tags) * 32 >= b - a) est_tags = n_tags_r;  // the estimate would not split
+            int64_t width = bm_pref ? (bm_words / est_tags) * 32
                                     : (int64_t)((double)(b - a) * 0.8 * (double)sm_elems / (double)acc);
             width = max(R, (width / R) * R);
+            if (width >= b - a) width = max(R, (((b - a) / 2) / R) * R);  // always make progress
             int64_t m = (b - a + width - 1) / width;
             if (m > 64) {
               m = 64;
@@ -2529,8 +2541,9 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       if (N == 0) {
         // empty key range (sparse units: rows far apart): every measure adds 0
       } else if (s_bm) {
-        bitmap_range(reinterpret_cast<uint32_t*>(ebuf), druns, rcnt, rka, nr, N, a, b, kbase, n_tags, Gr, P.T, abase,
-                     fbase, bd, gd, tpb, U, wmax, s_nonmono != 0, tag_mask, reinterpret_cast<int*>(hist),
+        bitmap_range(reinterpret_cast<uint32_t*>(ebuf), druns, rcnt, rka, nr, N, a, b, kbase,
+                     max(1, __popc(s_rtags & tag_mask)), Gr, P.T, abase,
+                     fbase, bd, gd, tpb, U, wmax, s_nonmono != 0, s_rtags & tag_mask, reinterpret_cast<int*>(hist),
                      kNW * 256);
         if (threadIdx.x < U.n_sub) atomicAdd(&hdr->acc[threadIdx.x], (unsigned long long)U.sub_val[threadIdx.x]);
         GVO_PH(if (threadIdx.x == 0) ph[6] += clock64() - t_r1;)
