@@ -64,10 +64,19 @@ constexpr int kSetsSmemBytes = kSetsCtasPerSm == 1 ? 222 * 1024 : kSetsCtasPerSm
 #define GVO_NOINL
 #endif
 
-#if GVO_SETS_CTAS_PER_SM != 1 && defined(GVO_SETS2_NT)
-constexpr int kNT = GVO_SETS2_NT;  // threads per CTA (experiment)
+// threads per CTA.  2 CTAs/SM: 320 threads (96 registers; A/B on C2:
+// 320 > 384 > 256 > 512, the 64-register build spills its stack to DRAM);
+// 1 CTA/SM: 512 (128 registers).
+#ifndef GVO_SETS2_NT
+#define GVO_SETS2_NT 320
+#endif
+#ifndef GVO_SETS1_NT
+#define GVO_SETS1_NT 512
+#endif
+#if GVO_SETS_CTAS_PER_SM != 1
+constexpr int kNT = GVO_SETS2_NT;
 #else
-constexpr int kNT = 512;           // threads per CTA
+constexpr int kNT = GVO_SETS1_NT;
 #endif
 constexpr int kNW = kNT / 32;
 constexpr int kMaxSrc = 64;        // sources per unit
