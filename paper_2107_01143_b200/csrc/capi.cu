@@ -98,7 +98,14 @@ struct gvo_ctx {
   int32_t seg_off = 0; // GVO_SEG=0 disables the segment cover (A/B hook)
   int32_t pat_off = 0; // GVO_PATTERN=0 disables pattern runs (A/B hook)
   int32_t fuse_warp = 1; // GVO_FUSE_WARP=0: warp statistics as their own launch
-  int64_t big_batch = 1024;  // batches of at least this many configs use the 1-CTA/SM set kernel (GVO_BIG_BATCH)
+  // Residency of the set kernel per batch: the 1-CTA/SM build (222 KB
+  // bitmaps) wins on batches of multi-field LBM-like templates (C4), the
+  // 2x320-thread build everywhere else (C2, C3, C5).  By default a batch of
+  // >= 1024 configs takes sets1 when every registered template has >= 3
+  // fields; GVO_BIG_BATCH=n forces sets1 for every batch of >= n configs.
+  int64_t big_batch = 1024;
+  bool big_forced = false;
+  bool all_wide = false;     // every registered template has >= 3 fields
   int32_t epoch = 0;     // set-kernel launch counter (queue readiness tag)
   DBuf<uint8_t> rank_scratch;
   // host-variant staging
@@ -171,7 +178,7 @@ int gvo_open(int device, gvo_ctx** out) {
   if (const char* e = getenv("GVO_SEG")) ctx->seg_off = atoi(e) == 0;
   if (const char* e = getenv("GVO_PATTERN")) ctx->pat_off = atoi(e) == 0;
   if (const char* e = getenv("GVO_FUSE_WARP")) ctx->fuse_warp = atoi(e) != 0;
-  if (const char* e = getenv("GVO_BIG_BATCH")) ctx->big_batch = atoll(e);
+  if (const char* e = getenv("GVO_BIG_BATCH")) { ctx->big_batch = atoll(e); ctx->big_forced = true; }
   ctx->n_ctas = kMaxSetsCtasPerSm * ctx->n_sm;
   *out = ctx;
   return GVO_OK;
@@ -289,6 +296,8 @@ int gvo_set_templates(gvo_ctx* ctx, const gvo_template* t, int32_t n) {
   ctx->max_acc = maxa;
   ctx->h_nacc = na;
   ctx->h_nfields = nf;
+  ctx->all_wide = !nf.empty();
+  for (int32_t f : nf) ctx->all_wide = ctx->all_wide && f >= 3;
   TplView& V = ctx->view;
   V.n_tpl = n;
   V.n_fields = ctx->t_nf.p; V.n_acc = ctx->t_na.p; V.acc_base = ctx->t_ab.p; V.field_base_off = ctx->t_fbo.p;
@@ -388,7 +397,7 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     WarpArgs WA{ctx->view, ctx->d_machines.p, cf, ctx->geos.p, ctx->coefs.p, nb * (S + 1), S, m0.sector_bytes,
                m0.bank_width_bytes, m0.l1_banks, 0, nullptr, cnt, stride, F,
                d_l1_access ? d_l1_access + b0 * l1_stride * 3 : nullptr, l1_stride, nullptr};
-    const bool big = nb >= ctx->big_batch;
+    const bool big = nb >= ctx->big_batch && (ctx->big_forced || ctx->all_wide);
     const bool fuse = ctx->fuse_warp &&
                       (int64_t)warp_item_smem(ctx->max_acc) <= (big ? sets1::sets_ebuf_bytes() : sets2::sets_ebuf_bytes());
     if (!fuse) {
