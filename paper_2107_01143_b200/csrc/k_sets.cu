@@ -43,7 +43,11 @@ constexpr int kSetsCtasPerSm = GVO_SETS2_CTAS;
 #else
 constexpr int kSetsCtasPerSm = GVO_SETS_CTAS_PER_SM;
 #endif
+#if GVO_SETS_CTAS_PER_SM != 1 && defined(GVO_SETS2_SMEM_KB)
+constexpr int kSetsSmemBytes = GVO_SETS2_SMEM_KB * 1024;  // experiment: leave more of the SM's 256 KB to L1
+#else
 constexpr int kSetsSmemBytes = kSetsCtasPerSm == 1 ? 222 * 1024 : kSetsCtasPerSm == 2 ? 110 * 1024 : 54 * 1024;
+#endif
 
 // per-CTA phase accounting for tools/unit_profile.py (build with
 // GVO_PHASE_STATS=1); compiled out of the product kernel
