@@ -97,6 +97,7 @@ struct gvo_ctx {
   int64_t sm_cap = 0;  // GVO_SMEM_ELEMS test hook
   int32_t seg_off = 0; // GVO_SEG=0 disables the segment cover (A/B hook)
   int32_t pat_off = 0; // GVO_PATTERN=0 disables pattern runs (A/B hook)
+  int32_t wave_fm = 1;  // GVO_WAVE_ORDER=0: wave units config-major instead of field-major
   int32_t fuse_warp = 1; // GVO_FUSE_WARP=0: warp statistics as their own launch
   // Residency of the set kernel per batch: the 1-CTA/SM build (222 KB
   // bitmaps) wins on batches of multi-field LBM-like templates (C4), the
@@ -177,6 +178,7 @@ int gvo_open(int device, gvo_ctx** out) {
   if (const char* e = getenv("GVO_SMEM_ELEMS")) ctx->sm_cap = atoll(e);
   if (const char* e = getenv("GVO_SEG")) ctx->seg_off = atoi(e) == 0;
   if (const char* e = getenv("GVO_PATTERN")) ctx->pat_off = atoi(e) == 0;
+  if (const char* e = getenv("GVO_WAVE_ORDER")) ctx->wave_fm = atoi(e) != 0;
   if (const char* e = getenv("GVO_FUSE_WARP")) ctx->fuse_warp = atoi(e) != 0;
   if (const char* e = getenv("GVO_BIG_BATCH")) { ctx->big_batch = atoll(e); ctx->big_forced = true; }
   ctx->n_ctas = kMaxSetsCtasPerSm * ctx->n_sm;
@@ -432,6 +434,7 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     L.sm_cap = ctx->sm_cap;
     L.seg_off = ctx->seg_off;
     L.pat_off = ctx->pat_off;
+    L.wave_field_major = ctx->wave_fm;
     if (fuse) {
       L.warp = WA;
       L.n_warp_items = WA.n_items;
@@ -581,6 +584,7 @@ int gvo_group_footprint(gvo_ctx* ctx, int32_t tpl, const int32_t block[3], const
     L.sm_cap = ctx->sm_cap;
     L.seg_off = ctx->seg_off;
     L.pat_off = ctx->pat_off;
+    L.wave_field_major = ctx->wave_fm;
   if (++ctx->epoch == 0) ++ctx->epoch;
   L.epoch = ctx->epoch;
   sets2::launch_sets(L, st);
@@ -648,6 +652,7 @@ int gvo_group_sets(gvo_ctx* ctx, int32_t tpl, const int32_t block[3], const int6
     L.sm_cap = ctx->sm_cap;
     L.seg_off = ctx->seg_off;
     L.pat_off = ctx->pat_off;
+    L.wave_field_major = ctx->wave_fm;
   if (++ctx->epoch == 0) ++ctx->epoch;
   L.epoch = ctx->epoch;
   sets2::launch_sets(L, st);

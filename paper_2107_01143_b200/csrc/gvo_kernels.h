@@ -60,6 +60,7 @@ struct SetsLaunch {
   int64_t sm_cap = 0;
   int32_t seg_off = 0;
   int32_t pat_off = 0;
+  int32_t wave_field_major = 1;
   int32_t epoch = 1;  // launch number, unique across both residencies (queue readiness tag)
 };
 namespace sets1 {

@@ -1562,6 +1562,7 @@ struct SetsArgs {
   int64_t sm_cap;           // test hook: cap on shared-memory elements (0 = none)
   int32_t seg_off;          // A/B hook: no segment cover
   int32_t pat_off;          // A/B hook: no pattern runs
+  int32_t wave_field_major; // wave units ordered field-major (heavy fields first)
   int32_t epoch;            // launch number; queue slots are ready when ready == epoch
 };
 
@@ -1997,8 +1998,10 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         bool skip = false;
         if (P.mode == 0) {
           if (item < n_wave_u) {
-            c = item / P.F_stride;
-            f = item % P.F_stride;
+            // field-major: every config's first field (the stencil source /
+            // pdf pull field: the heavy units) before the lighter ones
+            if (P.wave_field_major) { f = item / n_cfg_u; c = item % n_cfg_u; }
+            else { c = item / P.F_stride; f = item % P.F_stride; }
             j = P.S_req;
             stat_idx = item;
           } else {
@@ -2841,6 +2844,7 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st) {
   P.sm_cap = L.sm_cap;
   P.seg_off = L.seg_off;
   P.pat_off = L.pat_off;
+  P.wave_field_major = L.wave_field_major;
   P.epoch = L.epoch;  // never 0 (the zeroed initial state), unique per launch
   if (P.n_items + P.n_warp_items <= 0) return;
   cudaMemsetAsync(P.work, 0, sizeof(unsigned long long), st);
