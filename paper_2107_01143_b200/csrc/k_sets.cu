@@ -1023,7 +1023,10 @@ __device__ GVO_NOINL uint64_t* cta_sort(uint64_t* a, uint64_t* b, int64_t n, int
 // rescaled interval ends for every subset; warp and CTA exclusive max-scans
 // give each lane the running maximum R before its sub-chunk.  Pass 2: a
 // sequential walk adds max(0, hi - max(lo - 1, R)) per selected interval.
-constexpr int kSubGroup = 4;
+#ifndef GVO_SWEEP_GROUP
+#define GVO_SWEEP_GROUP 4
+#endif
+constexpr int kSubGroup = GVO_SWEEP_GROUP;  // subsets swept per pass (A/B: 4 = 6 > 12)
 __device__ GVO_NOINL void sweep(const uint64_t* e, int64_t n, UnitSh& U, int64_t* wmax /* kMaxSub*kNW */) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t chunk = (n + kNW - 1) / kNW;
