@@ -281,17 +281,19 @@ def run_device(args, rank, world):
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    order_pin = torch.zeros(n, dtype=torch.int64, pin_memory=True).numpy()
     for _ in range(e2e_steps):
+        if world == 1:  # the one-call sweep entry: evaluate + rank, one synchronisation
+            ctx.check(L.gvo_sweep_host(ctx.h, _native._ptr(cfg_np), n, C.byref(smp), F, _native._ptr(counts_h),
+                                       _native._ptr(stats_h), _native._ptr(rec_h), _native._ptr(order_pin)))
+            order_h = order_pin
+            continue
         ctx.check(L.gvo_eval_configs_host(ctx.h, _native._ptr(cfg_np), n, C.byref(smp), F, _native._ptr(counts_h),
                                           _native._ptr(stats_h), _native._ptr(rec_h), None, None, 0))
         rec_d = torch.from_numpy(rec_h).to(dev, non_blocking=False)
-        if world > 1:
-            dist.all_gather_into_tensor(g_rec, rec_d)
-            ctx.check(L.gvo_rank(ctx.h, C.c_void_p(g_rec.data_ptr()), C.c_void_p(g_cfgs.data_ptr()), n * world,
-                                 C.c_void_p(d_order.data_ptr()), C.c_void_p(sptr)))
-        else:
-            ctx.check(L.gvo_rank(ctx.h, C.c_void_p(rec_d.data_ptr()), C.c_void_p(d_cfgs.data_ptr()), n,
-                                 C.c_void_p(d_order.data_ptr()), C.c_void_p(sptr)))
+        dist.all_gather_into_tensor(g_rec, rec_d)
+        ctx.check(L.gvo_rank(ctx.h, C.c_void_p(g_rec.data_ptr()), C.c_void_p(g_cfgs.data_ptr()), n * world,
+                             C.c_void_p(d_order.data_ptr()), C.c_void_p(sptr)))
         order_h = d_order.cpu().numpy()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
@@ -299,7 +301,7 @@ def run_device(args, rank, world):
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = n_real * e2e_steps / float(te.item())
-    h2d = n * cfg_np.itemsize + n * _native.RECORD_LEN * 8
+    h2d = n * cfg_np.itemsize + (n * _native.RECORD_LEN * 8 if world > 1 else 0)
     d2h = n * stride * 8 + n * _native.stats_len(F) * 8 + n * _native.RECORD_LEN * 8 + n * world * 8
     del order_h
 

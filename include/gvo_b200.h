@@ -231,6 +231,15 @@ int gvo_eval_configs_host(gvo_ctx* ctx, const gvo_config* h_cfgs, int64_t n,
 int gvo_rank(gvo_ctx* ctx, const double* d_records, const gvo_config* d_cfgs,
              int64_t n, int64_t* d_order, void* stream);
 
+/* Evaluate and rank host configurations in one call (one synchronisation):
+ * the batch entry a sweep driver binds (perf.rank_sweep, perf.py:98-132).
+ * h_order[i] = index of the i-th ranked config; other outputs as
+ * gvo_eval_configs_host (h_stats may be NULL). */
+int gvo_sweep_host(gvo_ctx* ctx, const gvo_config* h_cfgs, int64_t n,
+                   const gvo_sampling* sampling, int32_t F,
+                   int64_t* h_counts, double* h_stats, double* h_records,
+                   int64_t* h_order);
+
 /* ---- fine-grained parity entry points ---- */
 
 /* One collaborative group given as runs of consecutive linear block

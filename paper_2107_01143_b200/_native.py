@@ -144,6 +144,7 @@ def lib():
             "gvo_eval_configs": (C.c_int, [P, P, i64, C.POINTER(Sampling), i32, P, P, P, P, P, i32, P]),
             "gvo_eval_configs_host": (C.c_int, [P, P, i64, C.POINTER(Sampling), i32, P, P, P, P, P, i32]),
             "gvo_rank": (C.c_int, [P, P, P, i64, P, P]),
+            "gvo_sweep_host": (C.c_int, [P, P, i64, C.POINTER(Sampling), i32, P, P, P, P]),
             "gvo_group_footprint": (C.c_int, [P, i32, C.POINTER(C.c_int32), p64, p64, p64, i32, i64, p64]),
             "gvo_group_sets": (C.c_int, [P, i32, C.POINTER(C.c_int32), p64, p64, p64, i32, i64, p64]),
             "gvo_l1_cycles": (C.c_int, [P, i32, C.POINTER(C.c_int32), p64, i64, i64, i64, p64]),
@@ -169,7 +170,7 @@ def lib():
 EXPORTED_SYMBOLS = (
     "gvo_abi_version", "gvo_open", "gvo_close", "gvo_last_error", "gvo_set_templates",
     "gvo_set_machines", "gvo_counts_stride_eff", "gvo_eval_configs", "gvo_eval_configs_host",
-    "gvo_rank", "gvo_group_footprint", "gvo_group_sets", "gvo_l1_cycles", "gvo_eval_addresses",
+    "gvo_rank", "gvo_sweep_host", "gvo_group_footprint", "gvo_group_sets", "gvo_l1_cycles", "gvo_eval_addresses",
     "gvo_assemble_host", "gvo_predict_host", "gvo_set_timing", "gvo_kernel_times", "gvo_int_peak",
     "gvo_debug_units", "gvo_format_ranking_csv",
 )

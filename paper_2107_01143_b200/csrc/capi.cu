@@ -111,7 +111,7 @@ struct gvo_ctx {
   DBuf<uint8_t> rank_scratch;
   // host-variant staging
   DBuf<gvo_config> s_cfgs;
-  DBuf<int64_t> s_counts, s_i64a, s_i64b, s_i64c;
+  DBuf<int64_t> s_counts, s_i64a, s_i64b, s_i64c, s_order;
   DBuf<double> s_stats, s_records, s_fd;
   DBuf<int32_t> s_i32;
   DBuf<unsigned long long> s_ull;
@@ -492,6 +492,34 @@ int gvo_eval_configs_host(gvo_ctx* ctx, const gvo_config* h_cfgs, int64_t n, con
   if (h_stats) CK(cudaMemcpyAsync(h_stats, ctx->s_stats.p, n * GVO_STATS_LEN(F) * 8, cudaMemcpyDeviceToHost, st));
   if (h_field_down) CK(cudaMemcpyAsync(h_field_down, ctx->s_fd.p, n * 4 * F * 8, cudaMemcpyDeviceToHost, st));
   if (h_l1_access) CK(cudaMemcpyAsync(h_l1_access, ctx->s_i64a.p, n * l1_stride * 3 * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return GVO_OK;
+}
+
+int gvo_sweep_host(gvo_ctx* ctx, const gvo_config* h_cfgs, int64_t n, const gvo_sampling* sampling, int32_t F,
+                   int64_t* h_counts, double* h_stats, double* h_records, int64_t* h_order) {
+  if (!ctx || !sampling || !h_cfgs || !h_counts || !h_records || !h_order || n < 0)
+    return set_err(ctx, GVO_ERR_INVALID, "invalid arguments%s");
+  CK(cudaSetDevice(ctx->device));
+  int S, W;
+  sampling_eff(sampling, &S, &W);
+  const int64_t stride = gvo_counts_stride(F, S, W);
+  cudaStream_t st = ctx->stream;
+  if (!ctx->s_cfgs.ensure(std::max<int64_t>(n, 1)) || !ctx->s_counts.ensure(std::max<int64_t>(n * stride, 1)) ||
+      !ctx->s_records.ensure(std::max<int64_t>(n * GVO_RECORD_LEN, 1)) ||
+      (h_stats && !ctx->s_stats.ensure(std::max<int64_t>(n * GVO_STATS_LEN(F), 1))) ||
+      !ctx->s_order.ensure(std::max<int64_t>(n, 1)))
+    return set_err(ctx, GVO_ERR_CUDA, "staging alloc failed%s");
+  CK(cudaMemcpyAsync(ctx->s_cfgs.p, h_cfgs, n * sizeof(gvo_config), cudaMemcpyHostToDevice, st));
+  int rc = gvo_eval_configs(ctx, ctx->s_cfgs.p, n, sampling, F, ctx->s_counts.p, h_stats ? ctx->s_stats.p : nullptr,
+                            ctx->s_records.p, nullptr, nullptr, 0, st);
+  if (rc) return rc;
+  rc = gvo_rank(ctx, ctx->s_records.p, ctx->s_cfgs.p, n, ctx->s_order.p, st);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(h_counts, ctx->s_counts.p, n * stride * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h_records, ctx->s_records.p, n * GVO_RECORD_LEN * 8, cudaMemcpyDeviceToHost, st));
+  if (h_stats) CK(cudaMemcpyAsync(h_stats, ctx->s_stats.p, n * GVO_STATS_LEN(F) * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h_order, ctx->s_order.p, n * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return GVO_OK;
 }

@@ -317,3 +317,29 @@ def test_rank_sweep_sharded_matches_rank_sweep():
     assert [k.key for k in kept2] == [k.key for k in kept]
     np.testing.assert_array_equal(order2, order)
     np.testing.assert_array_equal(rec2, rec)
+
+
+def test_sweep_host_matches_eval_and_rank():
+    """gvo_sweep_host (evaluate + rank in one call) == gvo_eval_configs_host
+    followed by the device ranking."""
+    from paper_2107_01143_b200 import _native
+
+    m = gvo.b200_preset()
+    fam = gvo.KernelFamily("stencil", (64, 64, 64), radius=2)
+    cfgs = list(gvo.enumerate_sweep(64, foldings=("none", "2z"))) + list(gvo.enumerate_sweep(512))
+    kept, kernels, res, order = gvo.perf.evaluate_sweep(fam, cfgs, m, skip_invalid=True)
+    batch = gvo._engine.Batch()
+    for cfg, (k, launch, flops) in zip(kept, kernels):
+        batch.add(k.fields, k.accesses, launch, flops, m, None, gvo._engine.FOLD_RANK[cfg.folding])
+    ca = batch.config_array()
+    ctx = _native.context()
+    n, F = len(ca), ctx.max_fields
+    S, W = _native.effective_sampling(5, 2)
+    stride = _native.counts_stride(F, S, W)
+    counts = np.zeros((n, stride), dtype=np.int64)
+    rec = np.zeros((n, _native.RECORD_LEN))
+    o = np.zeros(n, dtype=np.int64)
+    ctx.check(_native.lib().gvo_sweep_host(ctx.h, _native._ptr(ca), n, _native.C.byref(_native.Sampling(5, 2, 0, 7, 0)),
+                                           F, _native._ptr(counts), None, _native._ptr(rec), _native._ptr(o)))
+    np.testing.assert_array_equal(o, order)
+    np.testing.assert_array_equal(rec, res.records)
