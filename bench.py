@@ -1,23 +1,27 @@
 """Benchmark: kernel configurations evaluated per second (BASELINE.json metric).
 
-Workload (BASELINE.json configs[1]): the range-four 3D25pt
-star stencil on a 640^3 grid, full block-size sweep — every power-of-two
-block (X, Y <= 512, Z <= 64) with X*Y*Z <= 1024 threads, 264 shapes of which
-246 tile the grid (skip_invalid) — evaluated with the B200 machine
-parameters, default fits, block_samples=5, wave_samples=2, then ranked.
-A step = evaluate + rank the whole sweep.  With N GPUs each rank evaluates
-its own 246-config shard (the same sweep with field alignment 8*rank bytes,
-so every rank's configs are distinct), records are all-gathered over NCCL
-and the global ranking runs on the device (weak scaling).
+Workload (default): BASELINE.json configs[4], C5 — the combined stencil + LBM
+configuration space at B200 cache/HBM parameters, 1,205,184 configurations
+(paper_2107_01143_b200/workloads.py space_c5: the 3D25pt/13pt/19pt/7pt star
+stencils (r = 1..4) on 640^3 x every power-of-two block <= 1024 threads x
+folding {none, 2y, 2z} x layout {fzyx, zyxf} x {2, 4} components x 32 field
+alignments, and the two-phase LBM kernels (D3Q27 hydro + D3Q15 phase field)
+on 256^3 x 154 blocks x folding x layout x 16 alignments, each at L2
+capacity {full, 1/2, 1/4}), evaluated with block_samples=5, wave_samples=2
+and default fits, then ranked (perf.py:131 key).  It is the largest
+single-GPU space of BASELINE.json, so it is the headline.
 
---workload C1|C3|C4|C5 runs the other BASELINE.json configuration spaces
-(paper_2107_01143_b200/workloads.py): the space is dealt to ranks by
-estimated cost (shard.py), one NCCL all-gather of the records, device rank
-of the whole space (strong scaling: total work fixed).
+A step = evaluate + rank the whole space.  With N GPUs (torchrun) the space
+is dealt to ranks by estimated cost (shard.py; strong scaling: total work
+fixed), every rank evaluates its shard, one all-gather of the fixed-size
+records (+ their global index), and the device ranks the whole space in
+global order (gvo_rank_gathered: ties break by input order, padding dropped).
+
+--workload C1|C2|C3|C4 runs the other BASELINE.json spaces (parity cases).
 
 --impl reference times the reference's own CPU estimator (pip-installed
-unmodified under baseline/_ref; the CPU oracle port if that is missing) on a
-bounded sample of the same workload with all host cores.
+unmodified under baseline/_ref; the CPU oracle port if that is missing) on
+bounded seeded samples of the same workload with all host cores.
 """
 
 from __future__ import annotations
@@ -36,11 +40,13 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-GRID = (640, 640, 640)
-RADIUS = 4
-# kernels per step (one batch): k_setup, k_sets (warp statistics fused),
-# k_finish, k_rank_small (n <= 2048)
-LAUNCHES_PER_STEP = 4
+METRIC = "kernel configs evaluated/sec (1/2/4/8 B200) vs host-CPU reference; % int/HBM roofline"
+SEED = 20240811  # BASELINE.md §3 / SURVEY §8d seeded subsets
+CPU_SAMPLE = 512  # >= 500 configurations for the 1e5 / 1e6 spaces
+CPU_SAMPLE_1P = 12  # single-process rate: a bounded prefix of the same sample
+# ncu capture of the dominant kernel for the default workload (tools/ncu_capture.py)
+CAPTURE = ROOT / "profiles" / "r02_ncu_capture_c5.json"
+ISSUE_SLOTS_PER_SM = 4  # warp schedulers per SM (one warp-instruction issue per cycle each)
 
 
 def b200_machine():
@@ -49,10 +55,9 @@ def b200_machine():
     return gvo.b200_preset()
 
 
-# ---------------------------------------------------------------- device arm
 WORKLOADS = {
     "C1": "C1: 2D5pt Jacobi 256^2, block 32x4x1 (PR1 oracle config)",
-    "C2": "C2: 3D25pt r4 640^3 full power-of-two block sweep (246 valid configs/rank), "
+    "C2": "C2: 3D25pt r4 640^3 full power-of-two block sweep (246 valid configs), "
           "B200 machine params, samples 5/2, evaluate+rank",
     "C3": "C3: 3D25pt/13pt (r4/r2) 640^3 x folding x layout fzyx/zyxf x 2/4 components x 16 alignments "
           "(93,184 configs), B200 params, samples 5/2, evaluate+rank",
@@ -64,37 +69,13 @@ WORKLOADS = {
 
 
 def build_shard(workload: str, rank: int, world: int):
-    """(Space of this rank's shard, padded shard length m, real configs of
-    the whole job).  C2: every rank evaluates its own 246-config sweep
-    (alignment 8*rank; weak scaling).  Others: the space is dealt by cost
-    and padded to equal length for the all-gather (strong scaling)."""
+    """(whole space, this rank's global indices, padded shard length m).
+    The space is dealt by estimated cost (strong scaling)."""
     from paper_2107_01143_b200 import shard, workloads as W
 
-    m = b200_machine()
-    if workload == "C2":
-        sp = W.space_c2(m, GRID, RADIUS, alignment=8 * rank)
-        return sp, len(sp), len(sp) * world
-    sp = W.space(workload, m)
+    sp = W.space(workload, b200_machine())
     idx = shard.shard_indices(shard.config_cost(sp.block, sp.n_accesses()), world, rank)
-    mlen = shard.pad_to(len(sp), world)
-    if len(idx) < mlen:  # pad with this shard's own configs (evaluated, not counted)
-        idx = np.concatenate([idx, idx[: mlen - len(idx)]])
-    return sp.subset(idx), mlen, len(sp)
-
-
-def n_addr(sp, m) -> int:
-    """Brute-force address-granule evaluations the reference performs for the
-    configs of a space: blocks n_b*T*A (+ lines), L1 T*A,
-    waves U*B_w*T*A."""
-    t = sp.block.astype(np.int64).prod(axis=1)
-    per_sm = np.minimum(m.max_blocks_per_sm, m.max_threads_per_sm // t)
-    bw = m.sm_count * per_sm
-    total = sp.grid_dim.prod(axis=1)
-    nw = -(-total // bw)
-    u = np.where(nw == 1, 1, 3)
-    n_b = np.minimum(5, np.maximum(1, np.clip(sp.grid_dim - 2, 1, None).prod(axis=1)))
-    a = sp.n_accesses()
-    return int((n_b * t * a + t * a + u * np.minimum(bw, total) * t * a).sum())
+    return sp, idx, shard.pad_to(len(sp), world)
 
 
 class ClockSampler:
@@ -138,30 +119,18 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def cpu_jobs(sp, n, rng):
-    """n seeded-random (kind, spec dict, machine dict) jobs of a space."""
+# ---------------------------------------------------------------- CPU legs
+def _ref_kind():
+    return "reference" if (ROOT / "baseline" / "_ref" / "gvo").exists() else "port"
+
+
+def cpu_jobs(sp, pick):
+    """(kind, spec dict, machine dict) jobs of the configurations `pick`."""
     from paper_2107_01143_b200.gvo.kernels import kernel_to_dict
     from paper_2107_01143_b200.gvo.machine import machine_to_dict
 
     kind = _ref_kind()
-    pick = rng.choice(len(sp), size=min(n, len(sp)), replace=False)
     return [(kind, kernel_to_dict(sp.kernel(int(i))), machine_to_dict(sp.machine(int(i)))) for i in pick]
-
-
-def cpu_sample_rate(sp, workload):
-    """Reference CPU estimator on a bounded sample (multiprocessing pool)."""
-    import multiprocessing as mp
-
-    cores = len(os.sched_getaffinity(0))
-    jobs = cpu_jobs(sp, max(3 * cores, 24), np.random.default_rng(20240811))
-    with mp.get_context("spawn").Pool(min(cores, len(jobs))) as pool:
-        pool.map(_warm, range(min(cores, len(jobs))))  # imports outside the timed sample
-        t0 = time.perf_counter()
-        list(pool.imap_unordered(_cpu_eval, jobs, chunksize=1))
-        dt = time.perf_counter() - t0
-    return {"value": len(jobs) / dt, "unit": "configs/s", "cores": min(cores, len(jobs)), "kind": jobs[0][0],
-            "sample": f"{len(jobs)} seeded-random configs of the {workload} space, "
-                      f"reference evaluate_kernel (B200 params, samples 5/2), {dt:.1f} s"}
 
 
 def _warm(_):
@@ -171,25 +140,68 @@ def _warm(_):
     return 0
 
 
-def _ref_kind():
-    return "reference" if (ROOT / "baseline" / "_ref" / "gvo").exists() else "port"
-
-
 def _cpu_eval(arg):
     """One configuration through the reference's public API (kernel spec +
-    machine JSON, as its CLI/bindings take them), or the oracle port."""
+    machine JSON, as its CLI/bindings take them), or the oracle port:
+    (glups, limiter)."""
     kind, spec, mdict = arg
     if kind == "reference":
         sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
         import gvo as ref
         from gvo.machine import machine_from_dict as ref_machine
 
-        return ref.evaluate_kernel(ref.kernel_from_dict(spec), ref_machine(mdict)).glups
+        p = ref.evaluate_kernel(ref.kernel_from_dict(spec), ref_machine(mdict))
+        return p.glups, p.limiter
     from oracle import gvo_oracle as ora
     from paper_2107_01143_b200 import gvo
     from paper_2107_01143_b200.gvo.machine import machine_from_dict
 
-    return ora.evaluate_kernel(gvo.kernel_from_dict(spec), machine_from_dict(mdict))["glups"]
+    ev = ora.evaluate_kernel(gvo.kernel_from_dict(spec), machine_from_dict(mdict))
+    return ev["glups"], ev["limiter"]
+
+
+def cpu_baseline(sp, workload):
+    """The reference CPU estimator on CPU_SAMPLE seeded-random configurations
+    of the space with a process per host core, plus a single-process rate on
+    a prefix of the same sample.  Returns (cpu_baseline dict, sample indices,
+    reference (glups, limiter) per sampled config)."""
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0))
+    pick = np.random.default_rng(SEED).choice(len(sp), size=min(CPU_SAMPLE, len(sp)), replace=False)
+    jobs = cpu_jobs(sp, pick)
+    with mp.get_context("spawn").Pool(cores) as pool:
+        pool.map(_warm, range(cores))  # imports outside the timed sample
+        t0 = time.perf_counter()
+        ref = pool.map(_cpu_eval, jobs, chunksize=1)
+        dt = time.perf_counter() - t0
+    n1 = min(CPU_SAMPLE_1P, len(jobs))
+    with mp.get_context("spawn").Pool(1) as pool:
+        pool.map(_warm, [0])
+        t1 = time.perf_counter()
+        pool.map(_cpu_eval, jobs[:n1], chunksize=1)
+        dt1 = time.perf_counter() - t1
+    out = {"value": len(jobs) / dt, "unit": "configs/s", "cores": cores, "kind": jobs[0][0],
+           "single_process": {"value": n1 / dt1, "unit": "configs/s", "cores": 1, "configs": n1,
+                              "seconds": round(dt1, 2)},
+           "sample": f"{len(jobs)} configurations of the {workload} space drawn with "
+                     f"np.random.default_rng({SEED}) (BASELINE.md §3), unmodified reference evaluate_kernel "
+                     f"(B200 params, samples 5/2), multiprocessing pool of {cores}: {dt:.1f} s; "
+                     f"single process: the first {n1} of them, {dt1:.1f} s"}
+    return out, pick, ref
+
+
+# ---------------------------------------------------------------- device arm
+def _capture_for(workload: str, bid: str):
+    """The committed ncu capture of the dominant kernel for this workload,
+    if it was taken with this very library build (same gvo_build_id)."""
+    p = ROOT / "profiles" / f"r02_ncu_capture_{workload.lower()}.json"
+    if not p.exists():
+        return None, f"no capture {p.name}"
+    d = json.loads(p.read_text())
+    if d.get("build_id") != bid:
+        return None, f"{p.name} was taken with build {d.get('build_id')}, this library is {bid}"
+    return d, str(p.relative_to(ROOT))
 
 
 def run_device(args, rank, world):
@@ -198,47 +210,68 @@ def run_device(args, rank, world):
 
     from paper_2107_01143_b200 import _native
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % max(1, ndev))
     torch.cuda.set_device(dev)
+    nccl = world > 1 and dist.get_backend() == "nccl"
     ctx = _native.context()
     L = _native.lib()
-    sp, n, n_real = build_shard(args.workload, rank, world)
-    cfg_np = sp.config_array(ctx)
+    C = _native.C
+    sp, mine, m = build_shard(args.workload, rank, world)
+    N = len(sp)
+    cfg_all = sp.config_array(ctx)
     ctx.sync_registries()
+    cfg_np = np.ascontiguousarray(cfg_all[mine])
+    n = len(cfg_np)
     F = ctx.max_fields
     S, W = _native.effective_sampling(5, 2)
     smp = _native.Sampling(5, 2, 0, 7, 0)
     stride = _native.counts_stride(F, S, W)
+    R = _native.RECORD_LEN
     d_cfgs = torch.from_numpy(cfg_np.view(np.uint8).copy()).to(dev)
-    d_counts = torch.zeros((n, stride), dtype=torch.int64, device=dev)
-    d_stats = torch.zeros((n, _native.stats_len(F)), dtype=torch.float64, device=dev)
-    d_rec = torch.zeros((n, _native.RECORD_LEN), dtype=torch.float64, device=dev)
-    d_order = torch.zeros(n * world, dtype=torch.int64, device=dev)
-    if world > 1:
-        g_rec = torch.zeros((n * world, _native.RECORD_LEN), dtype=torch.float64, device=dev)
-        g_cfgs = torch.zeros(n * world * cfg_np.itemsize, dtype=torch.uint8, device=dev)
-        dist.all_gather_into_tensor(g_cfgs, d_cfgs)
+    d_counts = torch.zeros((max(n, 1), stride), dtype=torch.int64, device=dev)
+    d_stats = torch.zeros((max(n, 1), _native.stats_len(F)), dtype=torch.float64, device=dev)
+    d_rec = torch.zeros((max(m, 1), R), dtype=torch.float64, device=dev)
+    d_order = torch.zeros(N, dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
-    C = _native.C
+    if world > 1:
+        gidx = np.full(m, -1, dtype=np.int64)
+        gidx[:n] = mine
+        g_gidx = torch.from_numpy(np.concatenate(_gather_np(gidx, world))).to(dev)
+        g_rec = torch.zeros((m * world, R), dtype=torch.float64, device=dev)
+        d_cfg_all = torch.from_numpy(cfg_all.view(np.uint8).copy()).to(dev)
 
-    def step():
-        ctx.check(L.gvo_eval_configs(ctx.h, C.c_void_p(d_cfgs.data_ptr()), n, C.byref(smp), F,
-                                     C.c_void_p(d_counts.data_ptr()), C.c_void_p(d_stats.data_ptr()),
-                                     C.c_void_p(d_rec.data_ptr()), None, None, 0, C.c_void_p(sptr)))
+    def gather_rec(src):
+        if nccl:
+            dist.all_gather_into_tensor(g_rec, src)
+        else:  # gloo (test mode: several ranks on one GPU): host round trip
+            parts = [torch.empty((m, R), dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(parts, src.cpu())
+            g_rec.copy_(torch.cat(parts))
+
+    def rank_all():
         if world > 1:
-            dist.all_gather_into_tensor(g_rec, d_rec)
-            ctx.check(L.gvo_rank(ctx.h, C.c_void_p(g_rec.data_ptr()), C.c_void_p(g_cfgs.data_ptr()), n * world,
-                                 C.c_void_p(d_order.data_ptr()), C.c_void_p(sptr)))
+            gather_rec(d_rec)
+            ctx.check(L.gvo_rank_gathered(ctx.h, C.c_void_p(g_rec.data_ptr()), C.c_void_p(g_gidx.data_ptr()),
+                                          m * world, C.c_void_p(d_cfg_all.data_ptr()), N, None,
+                                          C.c_void_p(d_order.data_ptr()), C.c_void_p(sptr)))
         else:
             ctx.check(L.gvo_rank(ctx.h, C.c_void_p(d_rec.data_ptr()), C.c_void_p(d_cfgs.data_ptr()), n,
                                  C.c_void_p(d_order.data_ptr()), C.c_void_p(sptr)))
 
+    def step():
+        if n:
+            ctx.check(L.gvo_eval_configs(ctx.h, C.c_void_p(d_cfgs.data_ptr()), n, C.byref(smp), F,
+                                         C.c_void_p(d_counts.data_ptr()), C.c_void_p(d_stats.data_ptr()),
+                                         C.c_void_p(d_rec.data_ptr()), None, None, 0, C.c_void_p(sptr)))
+        rank_all()
+
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    status = d_counts[:, _native.C_STATUS].cpu().numpy()
+    status = d_counts[:n, _native.C_STATUS].cpu().numpy()
     assert (status == 0).all(), f"engine status {np.unique(status)}"
     L.gvo_set_timing(ctx.h, 1)
     L.gvo_kernel_times(ctx.h, None, None, 1)
@@ -261,95 +294,167 @@ def run_device(args, rank, world):
     kcnt = (C.c_int64 * 8)()
     L.gvo_kernel_times(ctx.h, kms, kcnt, 1)
     L.gvo_set_timing(ctx.h, 0)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    per_rank = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+        allr = _gather_np(np.array([ms]), world)
+        ms_all = [float(a[0]) for a in allr]
+    else:
+        ms_all = [ms]
+    ms_max = max(ms_all)
+    del per_rank
     ms_step = ms_max / args.steps
-    value = n_real * args.steps / (ms_max * 1e-3)
+    value = N * args.steps / (ms_max * 1e-3)
+    final_order = d_order.cpu().numpy()
 
     # ---- e2e through the C ABI with host buffers (copies inside the region)
-    # host buffers in pinned memory (the inputs a user stages for the DMA engines)
-    counts_h = torch.zeros((n, stride), dtype=torch.int64, pin_memory=True).numpy()
-    stats_h = torch.zeros((n, _native.stats_len(F)), dtype=torch.float64, pin_memory=True).numpy()
-    rec_h = torch.zeros((n, _native.RECORD_LEN), dtype=torch.float64, pin_memory=True).numpy()
-    cfg_pin = torch.empty(cfg_np.nbytes, dtype=torch.uint8, pin_memory=True).numpy()
-    cfg_pin[:] = cfg_np.view(np.uint8).reshape(-1)
-    cfg_np = cfg_pin.view(cfg_np.dtype).reshape(cfg_np.shape)
-    e2e_steps = max(3, args.steps // 2)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    order_pin = torch.zeros(n, dtype=torch.int64, pin_memory=True).numpy()
-    for _ in range(e2e_steps):
-        if world == 1:  # the one-call sweep entry: evaluate + rank, one synchronisation
-            ctx.check(L.gvo_sweep_host(ctx.h, _native._ptr(cfg_np), n, C.byref(smp), F, _native._ptr(counts_h),
-                                       _native._ptr(stats_h), _native._ptr(rec_h), _native._ptr(order_pin)))
-            order_h = order_pin
-            continue
-        ctx.check(L.gvo_eval_configs_host(ctx.h, _native._ptr(cfg_np), n, C.byref(smp), F, _native._ptr(counts_h),
-                                          _native._ptr(stats_h), _native._ptr(rec_h), None, None, 0))
-        rec_d = torch.from_numpy(rec_h).to(dev, non_blocking=False)
-        dist.all_gather_into_tensor(g_rec, rec_d)
-        ctx.check(L.gvo_rank(ctx.h, C.c_void_p(g_rec.data_ptr()), C.c_void_p(g_cfgs.data_ptr()), n * world,
-                             C.c_void_p(d_order.data_ptr()), C.c_void_p(sptr)))
-        order_h = d_order.cpu().numpy()
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = n_real * e2e_steps / float(te.item())
-    h2d = n * cfg_np.itemsize + (n * _native.RECORD_LEN * 8 if world > 1 else 0)
-    d2h = n * stride * 8 + n * _native.stats_len(F) * 8 + n * _native.RECORD_LEN * 8 + n * world * 8
-    del order_h
+    e2e = None
+    if not args.no_e2e:
+        counts_h = torch.zeros((max(n, 1), stride), dtype=torch.int64, pin_memory=True).numpy()
+        stats_h = torch.zeros((max(n, 1), _native.stats_len(F)), dtype=torch.float64, pin_memory=True).numpy()
+        rec_h = torch.zeros((max(m, 1), R), dtype=torch.float64, pin_memory=True).numpy()
+        cfg_pin = torch.empty(max(cfg_np.nbytes, 1), dtype=torch.uint8, pin_memory=True).numpy()
+        cfg_pin[: cfg_np.nbytes] = cfg_np.view(np.uint8).reshape(-1)
+        cfg_h = cfg_pin[: cfg_np.nbytes].view(cfg_np.dtype)
+        order_pin = torch.zeros(N, dtype=torch.int64, pin_memory=True).numpy()
+        e2e_steps = max(2, args.steps // 4)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            if world == 1:  # the one-call sweep entry: evaluate + rank, one synchronisation
+                ctx.check(L.gvo_sweep_host(ctx.h, _native._ptr(cfg_h), n, C.byref(smp), F, _native._ptr(counts_h),
+                                           _native._ptr(stats_h), _native._ptr(rec_h), _native._ptr(order_pin)))
+                continue
+            if n:
+                ctx.check(L.gvo_eval_configs_host(ctx.h, _native._ptr(cfg_h), n, C.byref(smp), F,
+                                                  _native._ptr(counts_h), _native._ptr(stats_h), _native._ptr(rec_h),
+                                                  None, None, 0))
+            d_rec.copy_(torch.from_numpy(rec_h), non_blocking=False)
+            rank_all()
+            order_pin[:] = d_order.cpu().numpy()
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        e2e_all = _gather_np(np.array([e2e_s]), world) if world > 1 else [np.array([e2e_s])]
+        e2e_value = N * e2e_steps / max(float(a[0]) for a in e2e_all)
+        h2d = n * cfg_np.itemsize + (m * R * 8 if world > 1 else 0)
+        d2h = n * stride * 8 + n * _native.stats_len(F) * 8 + n * R * 8 + N * 8
+        e2e = {"value": e2e_value, "unit": "configs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "steps": e2e_steps,
+               "path": "gvo_sweep_host (pinned host configs in, counts/stats/records/order out)" if world == 1
+               else "gvo_eval_configs_host per shard + all-gather + gvo_rank_gathered, order to host"}
+        if world == 1 and not np.array_equal(order_pin, final_order):
+            raise AssertionError("e2e ranking differs from the device-timed ranking")
 
+    if args.dump_order and rank == 0:
+        np.save(args.dump_order, final_order)
     if rank != 0:
         return
-    # ---- roofline: dominant kernel (interval-union engine) vs measured INT32 issue rate
     names = ("setup", "warp", "sets", "finish", "rank")
     kernel_ms = {names[i]: kms[i] / max(1, args.steps) for i in range(5)}
-    top = max(("setup", "warp", "sets", "finish"), key=lambda k: kernel_ms[k])
-    peak = C.c_double()
-    ctx.check(L.gvo_int_peak(ctx.h, C.byref(peak)))
-    n_addr_total = n_addr(sp, b200_machine())
-    k_int = 8
-    sets_s = kernel_ms["sets"] * 1e-3
-    achieved = k_int * n_addr_total / sets_s / 1e9
-    algo_bytes = n * (cfg_np.itemsize + stride * 8 + _native.stats_len(F) * 8 + _native.RECORD_LEN * 8)
-    cpu = cpu_sample_rate(sp, args.workload) if world == 1 and not args.no_cpu else None
+    launches = {names[i]: int(kcnt[i]) for i in range(5)}
+    clocks = clk.summary()
+    bid = _native.build_id()
+    roof = roofline(args, kernel_ms, launches, clocks, n, cfg_np.itemsize, stride, F, ms_step, bid)
+    cpu = None
+    parity = None
+    if world == 1 and not args.no_cpu:
+        cpu, pick, ref = cpu_baseline(sp, args.workload)
+        parity = same_run_parity(ctx, cfg_all, pick, ref, smp, F)
     line = {
-        "metric": "kernel configs evaluated/sec (1/2/4/8 B200) vs host-CPU reference; % int/HBM roofline",
+        "metric": METRIC,
         "value": value, "unit": "configs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak" if args.workload == "C2" else "strong", "vs_baseline": None,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "int64", "data": "synthetic (deterministic config-space enumeration)",
-        "config": {"workload": WORKLOADS[args.workload], "configs_total": n_real,
-                   "configs_per_rank": n, "parallelism": f"dp{world} (config shards, NCCL all-gather + device rank)",
-                   "l2": "flushed between timed steps (256 MiB write)"},
-        "e2e": {"value": e2e_value, "unit": "configs/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "config": {"workload": WORKLOADS[args.workload], "configs_total": N,
+                   "configs_per_rank_max": m, "parallelism": f"dp{world} (cost-dealt config shards, "
+                   f"{'NCCL' if nccl or world == 1 else 'gloo'} all-gather + device rank)",
+                   "l2": "flushed between timed steps (256 MiB write)", "batch": int(os.environ.get("GVO_BATCH", 16384))},
+        "e2e": e2e,
         "gpu_launches": int(sum(kcnt[i] for i in range(5))),
+        "launches_per_step": {k: v / max(1, args.steps) for k, v in launches.items()},
         "kernel_ms_per_step": kernel_ms,
-        "roofline": {"bound": "int", "kernel": "k_sets (interval-union engine)",
-                     "achieved": achieved, "peak": peak.value / 1e9, "unit": "Gop/s (int32, address-equivalent)",
-                     "frac": achieved / (peak.value / 1e9),
-                     "note": "achieved = 8 int ops x brute-force address-granules the reference enumerates "
-                             "(SURVEY §8d N_addr) / k_sets time; >1 means the lattice collapse does less work "
-                             "than enumeration. peak = measured INT32 issue rate (gvo_int_peak).",
-                     "hbm": {"achieved": algo_bytes / (ms_step * 1e-3) / 1e9, "peak": 6531.3, "unit": "GB/s",
-                             "frac": algo_bytes / (ms_step * 1e-3) / 1e9 / 6531.3},
-                     "traffic": _ncu_traffic(),
-                     "hw": _ncu_hw()},
+        "rank_ms": ms_all if world > 1 else None,
+        "roofline": roof,
         "cpu_baseline": cpu,
-        "clocks": clk.summary(),
+        "parity_same_run": parity,
+        "clocks": clocks,
+        "build_id": bid,
     }
     print(json.dumps(line), flush=True)
 
 
+def _gather_np(a: np.ndarray, world: int):
+    """All-gather a small host array over the default group (any backend)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dist.get_backend() == "nccl":
+        t = t.cuda()
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    return [p.cpu().numpy() for p in parts]
+
+
+def roofline(args, kernel_ms, launches, clocks, n, cfg_bytes, stride, F, ms_step, bid):
+    """Dominant kernel (the interval-union engine k_sets) against the
+    integer-issue roof: warp-instructions it issues per second vs
+    148 SMs x 4 schedulers x SM clock.  The instruction count and DRAM bytes
+    per launch come from an ncu capture of the same workload taken with this
+    very library build (tools/ncu_capture.py; build id checked), the time
+    from this run's CUDA events on the launching stream."""
+    from paper_2107_01143_b200 import _native
+
+    top = max(("setup", "sets", "finish", "rank"), key=lambda k: kernel_ms[k])
+    cap, src = _capture_for(args.workload, bid)
+    clk_mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+    peak = 148 * ISSUE_SLOTS_PER_SM * clk_mhz * 1e6  # warp-instructions / s
+    sets_s = kernel_ms["sets"] * 1e-3
+    R = _native.RECORD_LEN
+    algo_bytes = n * (cfg_bytes + stride * 8 + _native.stats_len(F) * 8 + R * 8)
+    out = {"bound": "int", "kernel": "k_sets (interval-union engine)", "dominant": top,
+           "kernel_share_of_step": kernel_ms["sets"] / ms_step if ms_step else None,
+           "unit": "warp-inst/s", "peak": peak,
+           "peak_note": f"148 SMs x {ISSUE_SLOTS_PER_SM} issue slots x {clk_mhz:.0f} MHz (median SM clock sampled "
+                        "in the timed region): the integer/control-flow issue roof of a kernel with no "
+                        "tensor-core or HBM-bound work",
+           "achieved": None, "frac": None, "traffic": None, "capture": src,
+           "hbm": {"algorithmic_bytes_per_step": algo_bytes, "achieved": algo_bytes / (ms_step * 1e-3) / 1e9,
+                   "peak": 6537.0, "unit": "GB/s", "frac": algo_bytes / (ms_step * 1e-3) / 1e9 / 6537.0}}
+    if cap is not None and sets_s > 0:
+        inst = cap["k_sets"]["inst_executed_per_step"]
+        out["achieved"] = inst / sets_s
+        out["frac"] = out["achieved"] / peak
+        out["inst_executed_per_step"] = inst
+        out["traffic"] = cap["k_sets"]["dram_bytes_per_launch"]
+        out["traffic_per_step"] = cap["k_sets"]["dram_bytes_per_step"]
+        out["ncu"] = {k: cap["k_sets"].get(k) for k in ("issue_active_pct", "launches_per_step",
+                                                          "share_of_step_ncu", "hw")}
+    return out
+
+
+def same_run_parity(ctx, cfg_all, pick, ref, smp, F):
+    """GPU records of the CPU-baseline sample vs the reference's results of
+    the same run: GLup/s bit-exact, limiter equal, subset ranking equal."""
+    from paper_2107_01143_b200 import _native
+
+    sub = np.ascontiguousarray(cfg_all[pick])
+    out = ctx.sweep_host(sub, 5, 2, 0, want_l1_access=False, want_field_down=False)
+    g = out["records"][:, -1]
+    lim = out["records"][:, -2].astype(int)
+    exact = sum(1 for i, (rg, rl) in enumerate(ref) if g[i] == rg and _native.LIMITERS[lim[i]] == rl)
+    fold = {0: "2y", 1: "2z", 2: "none"}
+    keys = sorted(range(len(ref)), key=lambda i: (-ref[i][0], tuple(int(v) for v in sub["block"][i]),
+                                                 fold[int(sub["fold_rank"][i])], i))
+    return {"configs": len(ref), "glups_bit_exact_and_limiter_equal": exact,
+            "subset_ranking_identical": bool(list(map(int, out["order"])) == keys),
+            "reference_kind": _ref_kind()}
+
+
 def run_reference(args, rank, world):
-    """The reference's own CPU estimator on bounded samples of the workload,
-    all host cores (rank 0 only under torchrun)."""
+    """The reference's own CPU estimator on bounded seeded samples of the
+    workload, all host cores (rank 0 only under torchrun)."""
     if rank != 0:
         return
     import multiprocessing as mp
@@ -357,17 +462,18 @@ def run_reference(args, rank, world):
     from paper_2107_01143_b200 import workloads as W
 
     cores = len(os.sched_getaffinity(0))
-    sp = W.space_c2(b200_machine(), GRID, RADIUS) if args.workload == "C2" else W.space(args.workload)
-    rng = np.random.default_rng(20240811)
+    sp = W.space(args.workload, b200_machine())
+    rng = np.random.default_rng(SEED)
     per_step = max(3 * cores, 24)
     times = []
     kind = _ref_kind()
     with mp.get_context("spawn").Pool(cores) as pool:
         pool.map(_warm, range(cores))
         for i in range(args.warmup + args.steps):
-            jobs = cpu_jobs(sp, per_step, rng)
+            pick = rng.choice(len(sp), size=min(per_step, len(sp)), replace=False)
+            jobs = cpu_jobs(sp, pick)
             t0 = time.perf_counter()
-            list(pool.imap_unordered(_cpu_eval, jobs, chunksize=1))
+            pool.map(_cpu_eval, jobs, chunksize=1)
             if i >= args.warmup:
                 times.append((len(jobs), time.perf_counter() - t0))
     n_done = sum(a for a, _ in times)
@@ -375,60 +481,31 @@ def run_reference(args, rank, world):
     value = n_done / secs
     line = {
         "impl": "reference",
-        "metric": "kernel configs evaluated/sec (1/2/4/8 B200) vs host-CPU reference; % int/HBM roofline",
+        "metric": METRIC,
         "value": value, "unit": "configs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": secs / len(times) * 1e3, "higher_is_better": True,
-        "scaling": "weak" if args.workload == "C2" else "strong", "vs_baseline": None,
+        "scaling": "strong", "vs_baseline": None,
         "dtype": "int64", "data": "synthetic (deterministic config-space enumeration)",
         "config": {"workload": WORKLOADS[args.workload], "per_step_sample": per_step},
         "cpu_baseline": {"value": value, "unit": "configs/s", "cores": cores, "kind": kind,
-                         "sample": f"{per_step} seeded-random configs per step of the {args.workload} space, "
-                                   "unmodified reference evaluate_kernel"},
+                         "sample": f"{per_step} configurations per step of the {args.workload} space "
+                                   f"(np.random.default_rng({SEED}) stream, {n_done} timed in total), "
+                                   "unmodified reference evaluate_kernel, process per core"},
         "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def _ncu_traffic():
-    """dram read+write bytes per k_sets launch from the committed ncu capture
-    (profiles/r01_ncu_k_sets.json), or None."""
-    p = ROOT / "profiles" / "r01_ncu_k_sets.json"
-    if not p.exists():
-        return None
-    d = json.loads(p.read_text())
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    tot = 0.0
-    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-        v, u = d[k]
-        tot += float(v) * scale.get(u, 1)
-    return tot
-
-
-def _ncu_hw():
-    """Hardware utilisation of the same k_sets launch from the committed ncu
-    capture: issue slots, ALU pipe, shared-memory wavefronts (the counters the
-    north star names), or None."""
-    p = ROOT / "profiles" / "r01_ncu_k_sets.json"
-    if not p.exists():
-        return None
-    d = json.loads(p.read_text())
-    pick = {"issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
-            "alu_pipe_pct": "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
-            "smem_wavefronts_pct": "l1tex__data_pipe_lsu_wavefronts_mem_shared.avg.pct_of_peak_sustained_elapsed",
-            "dram_pct": "dram__throughput.avg.pct_of_peak_sustained_elapsed"}
-    out = {k: float(d[v][0]) for k, v in pick.items() if v in d}
-    out["source"] = "profiles/r01_ncu_k_sets.json (ncu --set full, C2 bench k_sets launch)"
-    return out
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--no-cpu", action="store_true", help="skip the in-run CPU baseline")
-    ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
+    ap.add_argument("--workload", default="C5", choices=sorted(WORKLOADS))
+    ap.add_argument("--dump-order", default="", help="save the final global ranking (rank 0, .npy)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -439,8 +516,10 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        # GVO_BENCH_BACKEND=gloo: several ranks sharing one GPU (tests); NCCL otherwise
+        backend = os.environ.get("GVO_BENCH_BACKEND", "nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count()))
+        dist.init_process_group(backend)
     try:
         run_device(args, rank, world)
     finally:

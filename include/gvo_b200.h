@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define GVO_ABI_VERSION 1
+#define GVO_ABI_VERSION 2
 
 /* ---- status codes: map 1:1 onto the reference's exception classes ---- */
 enum gvo_status {
@@ -230,6 +230,31 @@ int gvo_eval_configs_host(gvo_ctx* ctx, const gvo_config* h_cfgs, int64_t n,
  * (Python's sort is stable, hence the trailing input index). */
 int gvo_rank(gvo_ctx* ctx, const double* d_records, const gvo_config* d_cfgs,
              int64_t n, int64_t* d_order, void* stream);
+
+/* gvo_sweep_host plus the optional per-field down volumes and per-access
+ * L1 outputs of gvo_eval_configs_host (either may be NULL): the one call
+ * behind the drop-in rank_sweep (perf.py:98-132). */
+int gvo_sweep_host_ex(gvo_ctx* ctx, const gvo_config* h_cfgs, int64_t n,
+                      const gvo_sampling* sampling, int32_t F,
+                      int64_t* h_counts, double* h_stats, double* h_records,
+                      double* h_field_down, int64_t* h_l1_access, int32_t l1_access_stride,
+                      int64_t* h_order);
+
+/* Multi-GPU ranking of all-gathered shard records: d_rows
+ * [n_rows][GVO_RECORD_LEN] as gathered rank-major, d_gidx[n_rows] the
+ * global configuration index of each row (-1: all-gather padding, dropped),
+ * d_cfgs [n_global] the whole space in global (input) order.  Rows are
+ * scattered to global order (into d_records_global when non-NULL, else
+ * library scratch) and ranked there, so ties break by the global input
+ * index exactly as the reference's stable sort (perf.py:131) and padded
+ * rows are never ranked.  Synchronises the stream (index validation). */
+int gvo_rank_gathered(gvo_ctx* ctx, const double* d_rows, const int64_t* d_gidx, int64_t n_rows,
+                      const gvo_config* d_cfgs, int64_t n_global, double* d_records_global,
+                      int64_t* d_order, void* stream);
+
+/* Build id of the loaded library: hash of the sources and compile flags
+ * (profiles/ captures are tagged with it). */
+const char* gvo_build_id(void);
 
 /* Evaluate and rank host configurations in one call (one synchronisation):
  * the batch entry a sweep driver binds (perf.rank_sweep, perf.py:98-132).

@@ -20,6 +20,7 @@ _HERE = Path(__file__).resolve().parent
 _VARIANT = os.environ.get("GVO_LIB_VARIANT", "")
 LIB_PATH = _HERE / (f"libgvo_b200_{_VARIANT}.so" if _VARIANT else "libgvo_b200.so")
 
+ABI_VERSION = 2  # include/gvo_b200.h GVO_ABI_VERSION
 GVO_MAX_FIELDS = 16
 GVO_MAX_ACCESSES = 1024
 GVO_MAX_BLOCK_SAMPLES = 32
@@ -145,6 +146,9 @@ def lib():
             "gvo_eval_configs_host": (C.c_int, [P, P, i64, C.POINTER(Sampling), i32, P, P, P, P, P, i32]),
             "gvo_rank": (C.c_int, [P, P, P, i64, P, P]),
             "gvo_sweep_host": (C.c_int, [P, P, i64, C.POINTER(Sampling), i32, P, P, P, P]),
+            "gvo_rank_gathered": (C.c_int, [P, P, P, i64, P, i64, P, P, P]),
+            "gvo_sweep_host_ex": (C.c_int, [P, P, i64, C.POINTER(Sampling), i32, P, P, P, P, P, i32, P]),
+            "gvo_build_id": (C.c_char_p, []),
             "gvo_group_footprint": (C.c_int, [P, i32, C.POINTER(C.c_int32), p64, p64, p64, i32, i64, p64]),
             "gvo_group_sets": (C.c_int, [P, i32, C.POINTER(C.c_int32), p64, p64, p64, i32, i64, p64]),
             "gvo_l1_cycles": (C.c_int, [P, i32, C.POINTER(C.c_int32), p64, i64, i64, i64, p64]),
@@ -157,12 +161,17 @@ def lib():
             "gvo_debug_units": (C.c_int, [P, C.c_int, P, i64, C.POINTER(C.c_int64)]),
             "gvo_format_ranking_csv": (C.c_int, [P, i64, P, C.c_char_p, P, i32, P, i64, C.POINTER(C.c_int64)]),
         }
+        L.gvo_abi_version.restype = C.c_int
+        L.gvo_abi_version.argtypes = []
+        if L.gvo_abi_version() != ABI_VERSION:
+            raise NativeUnavailable(f"{LIB_PATH.name} ABI version {L.gvo_abi_version()} != {ABI_VERSION}; rebuild it")
         for name, (res, args) in sig.items():
-            fn = getattr(L, name)
+            try:
+                fn = getattr(L, name)
+            except AttributeError as exc:
+                raise NativeUnavailable(f"{LIB_PATH.name} does not export {name}; rebuild it") from exc
             fn.restype = res
             fn.argtypes = args
-        if L.gvo_abi_version() != 1:
-            raise NativeUnavailable("libgvo_b200.so ABI version mismatch")
         _lib = L
         return L
 
@@ -170,7 +179,7 @@ def lib():
 EXPORTED_SYMBOLS = (
     "gvo_abi_version", "gvo_open", "gvo_close", "gvo_last_error", "gvo_set_templates",
     "gvo_set_machines", "gvo_counts_stride_eff", "gvo_eval_configs", "gvo_eval_configs_host",
-    "gvo_rank", "gvo_sweep_host", "gvo_group_footprint", "gvo_group_sets", "gvo_l1_cycles", "gvo_eval_addresses",
+    "gvo_rank", "gvo_sweep_host", "gvo_rank_gathered", "gvo_build_id", "gvo_sweep_host_ex", "gvo_group_footprint", "gvo_group_sets", "gvo_l1_cycles", "gvo_eval_addresses",
     "gvo_assemble_host", "gvo_predict_host", "gvo_set_timing", "gvo_kernel_times", "gvo_int_peak",
     "gvo_debug_units", "gvo_format_ranking_csv",
 )
@@ -369,6 +378,29 @@ class Context:
                 "field_down": fd, "l1_access": l1}
 
 
+    def sweep_host(self, cfgs: np.ndarray, block_samples: int, wave_samples: int, bpw_override: int,
+                   want_l1_access: bool = True, want_field_down: bool = True):
+        """Evaluate + rank host configurations in one call (gvo_sweep_host_ex)."""
+        self.sync_registries()
+        F = self.max_fields
+        S, W = effective_sampling(block_samples, wave_samples)
+        smp = Sampling(int(block_samples), int(wave_samples), int(bpw_override or 0), 7, 0)
+        n = len(cfgs)
+        cfgs = np.ascontiguousarray(cfgs, dtype=CONFIG_DTYPE)
+        counts = np.empty((n, counts_stride(F, S, W)), dtype=np.int64)
+        stats = np.empty((n, stats_len(F)), dtype=np.float64)
+        records = np.empty((n, RECORD_LEN), dtype=np.float64)
+        fd = np.zeros((n, 4, F), dtype=np.float64) if want_field_down else None
+        A = self.max_accesses
+        l1 = np.zeros((n, A, 3), dtype=np.int64) if want_l1_access else None
+        order = np.empty(n, dtype=np.int64)
+        self.check(lib().gvo_sweep_host_ex(
+            self.h, _ptr(cfgs), n, C.byref(smp), F, _ptr(counts), _ptr(stats), _ptr(records),
+            _ptr(fd) if fd is not None else None, _ptr(l1) if l1 is not None else None, A, _ptr(order)))
+        return {"F": F, "S": S, "W": W, "counts": counts, "stats": stats, "records": records,
+                "field_down": fd, "l1_access": l1, "order": order}
+
+
 _ctx: Context | None = None
 
 
@@ -502,6 +534,22 @@ def rank_device(d_records, d_cfgs, n: int, d_order, stream: int = 0):
     ctx = context()
     ctx.check(lib().gvo_rank(ctx.h, C.c_void_p(d_records), C.c_void_p(d_cfgs), int(n), C.c_void_p(d_order),
                              C.c_void_p(stream)))
+
+
+def rank_gathered(d_rows, d_gidx, n_rows: int, d_cfgs, n_global: int, d_records_global, d_order,
+                  stream: int = 0):
+    """Device ranking of all-gathered shard rows carrying their global index
+    (-1: padding) over the whole space in global order (gvo_rank_gathered)."""
+    ctx = context()
+    ctx.check(lib().gvo_rank_gathered(ctx.h, C.c_void_p(d_rows), C.c_void_p(d_gidx), int(n_rows),
+                                      C.c_void_p(d_cfgs), int(n_global),
+                                      C.c_void_p(d_records_global) if d_records_global else None,
+                                      C.c_void_p(d_order), C.c_void_p(stream)))
+
+
+def build_id() -> str:
+    """gvo_build_id() of the loaded library (hash of sources + flags)."""
+    return lib().gvo_build_id().decode()
 
 
 def rank_host(cfgs: np.ndarray, records: np.ndarray) -> np.ndarray:

@@ -112,7 +112,7 @@ struct gvo_ctx {
   // host-variant staging
   DBuf<gvo_config> s_cfgs;
   DBuf<int64_t> s_counts, s_i64a, s_i64b, s_i64c, s_order;
-  DBuf<double> s_stats, s_records, s_fd;
+  DBuf<double> s_stats, s_records, s_fd, s_gather;
   DBuf<int32_t> s_i32;
   DBuf<unsigned long long> s_ull;
   int64_t batch = 16384;
@@ -210,6 +210,7 @@ void gvo_close(gvo_ctx* ctx) {
   ctx->s_stats.release();
   ctx->s_records.release();
   ctx->s_fd.release();
+  ctx->s_gather.release();
   ctx->s_ull.release();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -496,9 +497,10 @@ int gvo_eval_configs_host(gvo_ctx* ctx, const gvo_config* h_cfgs, int64_t n, con
   return GVO_OK;
 }
 
-int gvo_sweep_host(gvo_ctx* ctx, const gvo_config* h_cfgs, int64_t n, const gvo_sampling* sampling, int32_t F,
-                   int64_t* h_counts, double* h_stats, double* h_records, int64_t* h_order) {
-  if (!ctx || !sampling || !h_cfgs || !h_counts || !h_records || !h_order || n < 0)
+int gvo_sweep_host_ex(gvo_ctx* ctx, const gvo_config* h_cfgs, int64_t n, const gvo_sampling* sampling, int32_t F,
+                      int64_t* h_counts, double* h_stats, double* h_records, double* h_field_down,
+                      int64_t* h_l1_access, int32_t l1_stride, int64_t* h_order) {
+  if (!ctx || !sampling || !h_cfgs || !h_counts || !h_records || !h_order || n < 0 || (h_l1_access && l1_stride < 1))
     return set_err(ctx, GVO_ERR_INVALID, "invalid arguments%s");
   CK(cudaSetDevice(ctx->device));
   int S, W;
@@ -508,20 +510,30 @@ int gvo_sweep_host(gvo_ctx* ctx, const gvo_config* h_cfgs, int64_t n, const gvo_
   if (!ctx->s_cfgs.ensure(std::max<int64_t>(n, 1)) || !ctx->s_counts.ensure(std::max<int64_t>(n * stride, 1)) ||
       !ctx->s_records.ensure(std::max<int64_t>(n * GVO_RECORD_LEN, 1)) ||
       (h_stats && !ctx->s_stats.ensure(std::max<int64_t>(n * GVO_STATS_LEN(F), 1))) ||
+      (h_field_down && !ctx->s_fd.ensure(std::max<int64_t>(n * 4 * F, 1))) ||
+      (h_l1_access && !ctx->s_i64a.ensure(std::max<int64_t>(n * l1_stride * 3, 1))) ||
       !ctx->s_order.ensure(std::max<int64_t>(n, 1)))
     return set_err(ctx, GVO_ERR_CUDA, "staging alloc failed%s");
   CK(cudaMemcpyAsync(ctx->s_cfgs.p, h_cfgs, n * sizeof(gvo_config), cudaMemcpyHostToDevice, st));
   int rc = gvo_eval_configs(ctx, ctx->s_cfgs.p, n, sampling, F, ctx->s_counts.p, h_stats ? ctx->s_stats.p : nullptr,
-                            ctx->s_records.p, nullptr, nullptr, 0, st);
+                            ctx->s_records.p, h_field_down ? ctx->s_fd.p : nullptr,
+                            h_l1_access ? ctx->s_i64a.p : nullptr, l1_stride, st);
   if (rc) return rc;
   rc = gvo_rank(ctx, ctx->s_records.p, ctx->s_cfgs.p, n, ctx->s_order.p, st);
   if (rc) return rc;
   CK(cudaMemcpyAsync(h_counts, ctx->s_counts.p, n * stride * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(h_records, ctx->s_records.p, n * GVO_RECORD_LEN * 8, cudaMemcpyDeviceToHost, st));
   if (h_stats) CK(cudaMemcpyAsync(h_stats, ctx->s_stats.p, n * GVO_STATS_LEN(F) * 8, cudaMemcpyDeviceToHost, st));
+  if (h_field_down) CK(cudaMemcpyAsync(h_field_down, ctx->s_fd.p, n * 4 * F * 8, cudaMemcpyDeviceToHost, st));
+  if (h_l1_access) CK(cudaMemcpyAsync(h_l1_access, ctx->s_i64a.p, n * l1_stride * 3 * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(h_order, ctx->s_order.p, n * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return GVO_OK;
+}
+
+int gvo_sweep_host(gvo_ctx* ctx, const gvo_config* h_cfgs, int64_t n, const gvo_sampling* sampling, int32_t F,
+                   int64_t* h_counts, double* h_stats, double* h_records, int64_t* h_order) {
+  return gvo_sweep_host_ex(ctx, h_cfgs, n, sampling, F, h_counts, h_stats, h_records, nullptr, nullptr, 0, h_order);
 }
 
 int gvo_rank(gvo_ctx* ctx, const double* d_records, const gvo_config* d_cfgs, int64_t n, int64_t* d_order,
@@ -536,6 +548,39 @@ int gvo_rank(gvo_ctx* ctx, const double* d_records, const gvo_config* d_cfgs, in
   tmark_end(ctx, 4, as_stream(stream), tb);
   CK(cudaGetLastError());
   return GVO_OK;
+}
+
+int gvo_rank_gathered(gvo_ctx* ctx, const double* d_rows, const int64_t* d_gidx, int64_t n_rows,
+                      const gvo_config* d_cfgs, int64_t n_global, double* d_records_global, int64_t* d_order,
+                      void* stream) {
+  if (!ctx || n_rows < 0 || n_global < 0 || (n_rows && (!d_rows || !d_gidx)) || (n_global && (!d_cfgs || !d_order)))
+    return set_err(ctx, GVO_ERR_INVALID, "invalid arguments%s");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = as_stream(stream);
+  double* out = d_records_global;
+  if (!out) {
+    if (!ctx->s_gather.ensure(std::max<int64_t>(n_global * GVO_RECORD_LEN, 1)))
+      return set_err(ctx, GVO_ERR_CUDA, "gather scratch alloc failed%s");
+    out = ctx->s_gather.p;
+  }
+  if (!ctx->status.ensure(4)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
+  unsigned int* bad = reinterpret_cast<unsigned int*>(ctx->status.p + 3);
+  CK(cudaMemsetAsync(bad, 0, sizeof(unsigned int), st));
+  launch_scatter_gathered(d_rows, d_gidx, n_rows, n_global, out, bad, st);
+  CK(cudaGetLastError());
+  unsigned int h_bad = 0;
+  CK(cudaMemcpyAsync(&h_bad, bad, sizeof h_bad, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h_bad) return set_err(ctx, GVO_ERR_INVALID, "gathered global index out of range%s");
+  return gvo_rank(ctx, out, d_cfgs, n_global, d_order, stream);
+}
+
+const char* gvo_build_id(void) {
+#ifdef GVO_BUILD_ID
+  return GVO_BUILD_ID;
+#else
+  return "unknown";
+#endif
 }
 
 // --------------------------------------------------------------- custom groups

@@ -92,5 +92,7 @@ int launch_int_peak(int n_sm, cudaStream_t st, double* ops_per_s);
 int64_t rank_scratch_bytes(int64_t n);
 void launch_rank(const double* d_records, const gvo_config* d_cfgs, int64_t n, int64_t* d_order,
                  void* d_scratch, cudaStream_t st);
+void launch_scatter_gathered(const double* d_rows, const int64_t* d_gidx, int64_t n_rows, int64_t n_global,
+                             double* d_out, unsigned int* d_bad, cudaStream_t st);
 
 }  // namespace gvo

@@ -149,6 +149,28 @@ __global__ void k_order_out(const uint32_t* idx, int64_t n, int64_t* order) {
   if (i < n) order[i] = idx[i];
 }
 
+// Multi-GPU ranking: rows gathered rank-major from every shard
+// carry their global configuration index (-1: all-gather padding).  Scatter
+// them back to global order so the stable sort breaks ties by the input
+// index exactly as perf.py:131 does, and padding never reaches the ranking.
+__global__ void k_scatter_gathered(const double* rows, const int64_t* gidx, int64_t n_rows, int64_t n_global,
+                                   double* out, unsigned int* bad) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = t / GVO_RECORD_LEN, c = t % GVO_RECORD_LEN;
+  if (r >= n_rows) return;
+  const int64_t g = gidx[r];
+  if (g < 0) return;
+  if (g >= n_global) { if (c == 0) atomicOr(bad, 1u); return; }
+  out[g * GVO_RECORD_LEN + c] = rows[r * GVO_RECORD_LEN + c];
+}
+
+void launch_scatter_gathered(const double* d_rows, const int64_t* d_gidx, int64_t n_rows, int64_t n_global,
+                             double* d_out, unsigned int* d_bad, cudaStream_t st) {
+  if (n_rows <= 0) return;
+  const int64_t tot = n_rows * GVO_RECORD_LEN;
+  k_scatter_gathered<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(d_rows, d_gidx, n_rows, n_global, d_out, d_bad);
+}
+
 int64_t rank_scratch_bytes(int64_t n) {
   const int64_t n_tiles = (n + kTile - 1) / kTile;
   return n * 8 * 3 + n * 4 * 2 + 256 * n_tiles * 4 + 1024;

@@ -4,11 +4,15 @@ torch.distributed (NCCL over NVLink/NVSwitch on a B200 box).
 Every rank validates the whole sweep on the host exactly as rank_sweep does
 (perf.py:115-121), deals the configurations by estimated cost
 (paper_2107_01143_b200.shard), evaluates its shard on its own GPU, and one
-all-gather of the fixed-size per-config records (the 37-double ranking
-record, include/gvo_b200.h GVO_R_*) precedes the device ranking of the
-gathered records with the reference's key (perf.py:131).  Every rank returns
-the same global order and records, bit-identical to a single-GPU rank_sweep
-of the same configurations.
+all-gather of fixed-size rows — the 37-double ranking record
+(include/gvo_b200.h GVO_R_*), the configuration's global index (-1 for the
+padding that equalises shard lengths) and its error header — precedes the
+device ranking of the whole space in global order (gvo_rank_gathered), so
+ties break by input order as the reference's stable sort does
+(perf.py:131).  Every rank returns the same global order and records,
+bit-identical to a single-GPU rank_sweep of the same configurations, and
+every rank raises the reference's exception for the first failing
+configuration (no rank is left waiting in the collective).
 """
 
 from __future__ import annotations
@@ -21,7 +25,10 @@ from .. import _native, shard
 from . import _engine
 from .kernels import KernelFamily, SweepConfig
 from .machine import MachineDescriptor
-from .perf import PerfError, evaluate_sweep
+from .perf import PerfError, SweepPlan
+
+# error header columns gathered with every row (what raise_for_status reads)
+_HDR = (_native.C_STATUS, _native.C_ERR_PHASE, _native.C_ERR_GROUP, _native.C_ERR_ACCESS, _native.C_FIRSTWAVE)
 
 
 def rank_sweep_sharded(family: KernelFamily, configs: Iterable[SweepConfig], machine: MachineDescriptor,
@@ -30,55 +37,63 @@ def rank_sweep_sharded(family: KernelFamily, configs: Iterable[SweepConfig], mac
                        group=None):
     """(kept configs, order, records): the sweep's valid configurations in
     input order, their global ranking (indices into kept) and their ranking
-    records [len(kept)][RECORD_LEN], identical on every rank."""
+    records [len(kept)][RECORD_LEN], identical on every rank of ``group``."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    configs = list(configs)
-    if not configs:
+    plan = SweepPlan(family, configs, machine, fit_params, skip_invalid=skip_invalid)
+    n = len(plan)
+    if n == 0:
+        plan.raise_first_error(None, machine, block_samples, wave_samples, override_blocks_per_wave)
         raise PerfError("empty sweep")
-    kept, blocks, n_acc = [], [], []
-    templates: dict = {}
-    for cfg in configs:  # the same validation on every rank: identical kept lists
-        try:
-            launch, _ = family.launch_of(cfg)
-            key = family.template_key(cfg)
-            if key not in templates:
-                templates[key] = family.build(cfg)
-        except ValueError:
-            if skip_invalid:
-                continue
-            raise
-        kept.append(cfg)
-        blocks.append(launch.block_dim)
-        n_acc.append(len(templates[key].accesses))
-    n = len(kept)
-    mine = shard.shard_indices(shard.config_cost(np.asarray(blocks), np.asarray(n_acc)), world, rank)
+    n_acc = np.array([len(t[0].accesses) for t in plan.templates], dtype=np.int64)[plan.tpl]
+    mine = shard.shard_indices(shard.config_cost(plan.block, n_acc), world, rank)
     m = shard.pad_to(n, world)
-    dev = torch.device("cuda", _native.context().device)
-    local = torch.zeros((m, _native.RECORD_LEN + 1), dtype=torch.float64, device=dev)
-    local[:, -1] = -1.0  # global index column (-1: padding)
+    ctx = _native.context()
+    dev = torch.device("cuda", ctx.device)
+    R, H = _native.RECORD_LEN, len(_HDR)
+    local = np.zeros((m, R + 1 + H), dtype=np.float64)
+    local[:, R] = -1.0  # global index column (-1: padding)
+    cfg_all = plan.config_array()
     if len(mine):
-        _, _, res, _ = evaluate_sweep(family, [kept[i] for i in mine], machine, fit_params,
-                                      block_samples=block_samples, wave_samples=wave_samples,
-                                      override_blocks_per_wave=override_blocks_per_wave)
-        local[: len(mine), :-1] = torch.from_numpy(np.ascontiguousarray(res.records)).to(dev)
-        local[: len(mine), -1] = torch.from_numpy(mine.astype(np.float64)).to(dev)
-    gathered = shard.gather_records(local, world) if world > 1 else local
-    idx = gathered[:, -1].to(torch.int64)
-    keep = idx >= 0
-    records = torch.empty((n, _native.RECORD_LEN), dtype=torch.float64, device=dev)
-    records[idx[keep]] = gathered[keep, :-1]
-    # device ranking of all records (tie-break on block dims / folding as perf.py:131)
-    batch = _engine.Batch()
-    for cfg, b in zip(kept, blocks):
-        launch, flops = family.launch_of(cfg)
-        k = templates[family.template_key(cfg)]
-        batch.add(k.fields, k.accesses, launch, flops, machine, fit_params, _engine.FOLD_RANK[cfg.folding])
-    cf = torch.from_numpy(np.ascontiguousarray(batch.config_array()).view(np.uint8).copy()).to(dev)
+        out = ctx.eval_configs_host(cfg_all[mine], block_samples, wave_samples, override_blocks_per_wave or 0,
+                                    want_field_down=False)
+        local[: len(mine), :R] = out["records"]
+        local[: len(mine), R] = mine
+        local[: len(mine), R + 1:] = out["counts"][:, list(_HDR)]
+    # gloo gathers host tensors, NCCL device tensors
+    backend = dist.get_backend(group) if dist.is_initialized() else "none"
+    t_local = torch.from_numpy(local)
+    if backend == "nccl":
+        t_local = t_local.to(dev)
+    gathered = shard.gather_records(t_local, world, group) if world > 1 else t_local
+    g = gathered.cpu().numpy()
+    gidx = g[:, R].astype(np.int64)
+    # the reference raises at the first failing configuration: every rank
+    # sees every row's status, so every rank raises the same exception
+    status = np.zeros(n, dtype=np.int64)
+    valid = gidx >= 0
+    status[gidx[valid]] = g[valid, R + 1].astype(np.int64)
+    if status.any() or plan.build_error is not None:
+        i = int(np.flatnonzero(status)[0]) if status.any() else None
+        if i is not None:
+            row = g[np.flatnonzero(gidx == i)[0]]
+            counts = np.zeros((1, _native.C_HDR), dtype=np.int64)
+            counts[0, list(_HDR)] = row[R + 1:].astype(np.int64)
+            res = _engine.Result(0, 0, 0, counts, None, None, None, None)
+            k, launch, _ = plan.kernel_row(i)
+            _engine.raise_for_status(res, 0, k.with_launch(launch), machine, block_samples, wave_samples,
+                                     override_blocks_per_wave)
+        raise plan.build_error[1]
+    # device ranking of the whole space in global order
+    d_rows = torch.from_numpy(np.ascontiguousarray(g[:, :R])).to(dev)
+    d_gidx = torch.from_numpy(gidx.copy()).to(dev)
+    d_cfg = torch.from_numpy(cfg_all.view(np.uint8).copy()).to(dev)
+    records = torch.empty((n, R), dtype=torch.float64, device=dev)
     order = torch.empty(n, dtype=torch.int64, device=dev)
-    _native.rank_device(records.data_ptr(), cf.data_ptr(), n, order.data_ptr(),
-                        torch.cuda.current_stream(dev).cuda_stream)
-    return kept, order.cpu().numpy(), records.cpu().numpy()
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    _native.rank_gathered(d_rows.data_ptr(), d_gidx.data_ptr(), len(gidx), d_cfg.data_ptr(), n,
+                          records.data_ptr(), order.data_ptr(), stream)
+    return plan.configs, order.cpu().numpy(), records.cpu().numpy()

@@ -165,6 +165,49 @@ def grid_iteration(kernel: KernelDescriptor, group: CollaborativeGroup, granular
     return FootprintResult(granularity, per_field)
 
 
+def naive_footprint_oracle(kernel: KernelDescriptor, group: CollaborativeGroup, granularity: int,
+                           kinds: Iterable[str] | None = None) -> FootprintResult:
+    """Brute-force twin of grid_iteration (reference footprint.py:474-507):
+    every thread's address evaluated by the device bytecode interpreter
+    (gvo_eval_addresses), granules deduplicated per field/kind and per
+    (block, warp) on the device.  Independent of the interval engine, so the
+    two cross-check each other exactly as in the reference's tests."""
+    import torch
+
+    kinds = _check_kinds(granularity, kinds)
+    bx, by, bz = kernel.launch.block_dim
+    s = bx * by * bz
+    xs, ys, zs = group.block_coords()
+    t = np.arange(s, dtype=np.int64)
+    nb = len(xs)
+    coords = np.empty((nb * s, 6), dtype=np.int64)
+    coords[:, 0] = np.tile(t % bx, nb)
+    coords[:, 1] = np.tile((t // bx) % by, nb)
+    coords[:, 2] = np.tile(t // (bx * by), nb)
+    coords[:, 3] = np.repeat(np.asarray(xs, dtype=np.int64), s)
+    coords[:, 4] = np.repeat(np.asarray(ys, dtype=np.int64), s)
+    coords[:, 5] = np.repeat(np.asarray(zs, dtype=np.int64), s)
+    dev = torch.device("cuda", _native.context().device)
+    idx = torch.arange(nb * s, dtype=torch.int64, device=dev)
+    warp_key = (idx // s) * ((s + 31) // 32) + (idx % s) // 32
+    bases = kernel.base_substitution
+    per_field = {}
+    for f in kernel.fields:
+        for kind in kinds:
+            accesses = [a for a in kernel.accesses if a.field == f.name and a.kind == kind]
+            if not accesses:
+                continue
+            allg, total = [], 0
+            for a in accesses:
+                addr = torch.from_numpy(_native.eval_addresses(a.expr, bases, kernel.launch.block_dim, coords)).to(dev)
+                gran = torch.div(addr, granularity, rounding_mode="floor")
+                allg.append(gran)
+                pairs = torch.stack([warp_key, gran], dim=1)
+                total += a.multiplicity * int(torch.unique(pairs, dim=0).shape[0])
+            per_field[(f.name, kind)] = KindCounts(int(torch.unique(torch.cat(allg)).numel()), total)
+    return FootprintResult(granularity, per_field)
+
+
 # ---------------------------------------------------------------------------
 # waves
 

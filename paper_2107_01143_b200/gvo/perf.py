@@ -96,38 +96,161 @@ class SweepRow:
     prediction: PerfPrediction
 
 
+_FOLD_FACTORS = {"none": (1, 1, 1), "2y": (1, 2, 1), "2z": (1, 1, 2)}
+
+
+class SweepPlan:
+    """A validated sweep in columnar form: the kept configurations (input
+    order), one device template per distinct access structure and the
+    gvo_config array, built without one descriptor per configuration.
+
+    Validation follows the reference loop (perf.py:115-121): build errors
+    (ValueError from family.build) skip the configuration with
+    ``skip_invalid`` and otherwise stop the sweep at the first invalid
+    configuration.  Stencil / LBM families validate the whole batch with
+    array arithmetic; any configuration the vector check does not accept
+    goes through family.launch_of, which raises exactly what build raises.
+    """
+
+    def __init__(self, family: KernelFamily, configs, machine, fit_params=None, *, skip_invalid=False):
+        self.family = family
+        configs = list(configs)
+        if not configs:
+            raise PerfError("empty sweep")
+        ctx = _native.context()
+        self.machine_id = ctx.machine_id(machine, fit_params)
+        n = len(configs)
+        block = np.zeros((n, 3), dtype=np.int64)
+        grid = np.zeros((n, 3), dtype=np.int64)
+        wpt = np.ones(n, dtype=np.int64)
+        flops = np.zeros(n, dtype=np.int64)
+        tkey = [None] * n
+        fast = np.zeros(n, dtype=bool)
+        if family.kind in ("stencil", "lbm") and len(tuple(family.grid)) == 3:
+            try:
+                b = np.array([c.block_dim for c in configs], dtype=np.int64)
+                ok_shape = b.shape == (n, 3)
+            except (TypeError, ValueError):
+                ok_shape = False
+            if ok_shape:
+                ff = np.array([_FOLD_FACTORS.get(c.folding, (0, 0, 0)) if isinstance(c.folding, str) else (0, 0, 0)
+                               for c in configs], dtype=np.int64)
+                g = np.array([int(v) for v in family.grid], dtype=np.int64)
+                eff = b * ff
+                ok = (ff > 0).all(axis=1) & (b >= 1).all(axis=1) & (g >= 1).all()
+                ok &= ((g[None, :] % np.where(eff > 0, eff, 1)) == 0).all(axis=1)
+                if family.kind == "stencil":
+                    ok &= family.radius >= 1
+                    fl = 6 * family.radius + 1
+                else:
+                    ok &= ff.prod(axis=1) == 1  # lbm: folding "none" only
+                    fl = 250 if family.flops_per_lup is None else family.flops_per_lup
+                fast = ok
+                block[ok] = b[ok]
+                grid[ok] = g[None, :] // np.where(eff[ok] > 0, eff[ok], 1)
+                wpt[ok] = ff[ok].prod(axis=1)
+                flops[ok] = fl
+                for i in np.flatnonzero(ok):
+                    tkey[i] = family.template_key(configs[i])
+        self.build_error = None  # (index, exception) of the first invalid config (skip_invalid=False)
+        keep = np.ones(n, dtype=bool)
+        for i in np.flatnonzero(~fast):
+            cfg = configs[i]
+            try:
+                launch, fl = family.launch_of(cfg)
+                tkey[i] = family.template_key(cfg)
+            except ValueError as exc:
+                keep[i] = False
+                if skip_invalid:
+                    continue
+                self.build_error = (int(i), exc)
+                keep[i:] = False  # the reference loop stops here
+                break
+            block[i], grid[i], wpt[i], flops[i] = launch.block_dim, launch.grid_dim, launch.work_per_thread, fl
+        idx = np.flatnonzero(keep)
+        self.configs = [configs[i] for i in idx]
+        self.block, self.grid, self.wpt, self.flops = block[idx], grid[idx], wpt[idx], flops[idx]
+        # one template per key (built from its first configuration), ids registered once
+        self.templates: list = []
+        tix: dict = {}
+        self.tpl = np.zeros(len(idx), dtype=np.int32)
+        for j, i in enumerate(idx):
+            t = tix.get(tkey[i])
+            if t is None:
+                t = tix[tkey[i]] = len(self.templates)
+                k = family.build(configs[i])
+                self.templates.append((k, ctx.template_id(k.fields, k.accesses)))
+            self.tpl[j] = t
+        self.fold_rank = np.array([_engine.FOLD_RANK[c.folding] for c in self.configs], dtype=np.int32)
+
+    def __len__(self) -> int:
+        return len(self.configs)
+
+    def config_array(self) -> np.ndarray:
+        a = np.zeros(len(self), dtype=_native.CONFIG_DTYPE)
+        tid = np.array([t[1] for t in self.templates], dtype=np.int32)
+        a["template_id"] = tid[self.tpl] if len(self) else 0
+        a["machine_id"] = self.machine_id
+        a["block"] = self.block
+        a["fold_rank"] = self.fold_rank
+        a["grid"] = self.grid
+        a["work_per_thread"] = self.wpt
+        a["flops_per_lup"] = self.flops
+        return a
+
+    def kernel_row(self, i: int):
+        """(template descriptor, LaunchConfig, flops) of kept config i."""
+        from .kernels import LaunchConfig
+
+        k = self.templates[int(self.tpl[i])][0]
+        launch = LaunchConfig(tuple(int(v) for v in self.block[i]), tuple(int(v) for v in self.grid[i]),
+                              int(self.wpt[i]))
+        return k, launch, int(self.flops[i])
+
+    def raise_first_error(self, res, machine, block_samples, wave_samples, override):
+        """Reference order: the first configuration that fails (to evaluate,
+        or to build) raises; evaluation errors of earlier configs first."""
+        bad = np.flatnonzero(res.counts[:, _native.C_STATUS]) if res is not None else []
+        if len(bad):
+            i = int(bad[0])
+            k, launch, _ = self.kernel_row(i)
+            _engine.raise_for_status(res, i, k.with_launch(launch), machine, block_samples, wave_samples, override)
+        if self.build_error is not None:
+            raise self.build_error[1]
+
+
+class _KernelRows(Sequence):
+    """(descriptor, launch, flops) per kept configuration, built on access."""
+
+    def __init__(self, plan: SweepPlan):
+        self._plan = plan
+
+    def __len__(self) -> int:
+        return len(self._plan)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self._plan.kernel_row(j) for j in range(*i.indices(len(self)))]
+        return self._plan.kernel_row(i)
+
+
 def evaluate_sweep(family: KernelFamily, configs: Iterable[SweepConfig], machine: MachineDescriptor,
                    fit_params=None, *, block_samples=5, wave_samples=2, override_blocks_per_wave=None,
                    skip_invalid=False):
-    """Batched evaluation: (kept configs, per-config descriptors' field names,
-    device result, ranking order).  Validation errors follow perf.py:115-121."""
-    configs = list(configs)
-    if not configs:
+    """Batched evaluation: (kept configs, per-config (descriptor, launch,
+    flops) rows, device result, ranking order).  One columnar batch, one
+    evaluate + rank call (gvo_sweep_host_ex); validation and error order
+    follow perf.py:115-130."""
+    plan = SweepPlan(family, configs, machine, fit_params, skip_invalid=skip_invalid)
+    if not len(plan):
+        plan.raise_first_error(None, machine, block_samples, wave_samples, override_blocks_per_wave)
         raise PerfError("empty sweep")
-    batch = _engine.Batch()
-    templates: dict = {}
-    kept, kernels = [], []
-    for cfg in configs:
-        try:
-            launch, flops = family.launch_of(cfg)
-            key = family.template_key(cfg)
-            if key not in templates:
-                templates[key] = family.build(cfg)
-        except ValueError:
-            if skip_invalid:
-                continue
-            raise
-        k = templates[key]
-        batch.add(k.fields, k.accesses, launch, flops, machine, fit_params, _engine.FOLD_RANK[cfg.folding])
-        kept.append(cfg)
-        kernels.append((k, launch, flops))
-    res = batch.run(block_samples, wave_samples, override_blocks_per_wave, phases=7, want_l1=True)
-    for i, (k, launch, flops) in enumerate(kernels):
-        if res.counts[i, _native.C_STATUS]:
-            _engine.raise_for_status(res, i, k.with_launch(launch), machine, block_samples, wave_samples,
-                                     override_blocks_per_wave)
-    order = _native.rank_host(batch.config_array(), res.records)
-    return kept, kernels, res, order
+    ctx = _native.context()
+    out = ctx.sweep_host(plan.config_array(), block_samples, wave_samples, override_blocks_per_wave or 0)
+    res = _engine.Result(out["F"], out["S"], out["W"], out["counts"], out["stats"], out["records"],
+                         out["field_down"], out["l1_access"])
+    plan.raise_first_error(res, machine, block_samples, wave_samples, override_blocks_per_wave)
+    return plan.configs, _KernelRows(plan), res, out["order"]
 
 
 class SweepRows(Sequence):

@@ -33,18 +33,18 @@ def pad_to(n: int, world: int) -> int:
     return -(-n // world)
 
 
-def gather_records(local, world: int):
-    """All-gather a [m][k] records tensor (equal m on every rank) into
-    [world*m][k] with torch.distributed (one collective)."""
+def gather_records(local, world: int, group=None):
+    """All-gather a [m][k] records tensor (equal m on every rank of
+    ``group``) into [world*m][k] with torch.distributed (one collective)."""
     import torch
     import torch.distributed as dist
 
     out = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     if hasattr(dist, "all_gather_into_tensor") and local.is_cuda:
-        dist.all_gather_into_tensor(out, local.contiguous())
+        dist.all_gather_into_tensor(out, local.contiguous(), group=group)
     else:
         parts = list(out.chunk(world, dim=0))
-        dist.all_gather(parts, local.contiguous())
+        dist.all_gather(parts, local.contiguous(), group=group)
         out = torch.cat(parts, dim=0)
     return out
 

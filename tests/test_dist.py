@@ -71,3 +71,104 @@ def test_gloo_world2_all_gather_reassembles_every_config():
     assert sorted(gi[valid].tolist()) == list(range(n))
     assert np.array_equal(g0[valid, 0], gi[valid].astype(float))
     assert np.array_equal(g0[valid, 1], gi[valid] * 7 + 1.0)
+
+
+# ------------------------------------------------------------------ GPU: the real engine, two ranks
+def _engine_worker(rank, world, port, out_q, case):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)  # every rank shares the one GPU of the test box
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2107_01143_b200 import gvo
+
+    try:
+        m = gvo.b200_preset()
+        fam = gvo.KernelFamily("stencil", (64, 64, 64), radius=2)
+        cfgs = list(gvo.enumerate_sweep(64, foldings=("none", "2y", "2z"))) + list(gvo.enumerate_sweep(512))
+        group = None
+        if case == "subgroup":
+            group = dist.new_group([0, 2])
+            if rank == 1:
+                out_q.put((rank, None, None, None))
+                return
+        if case == "error":
+            cfgs = cfgs[:40] + [gvo.SweepConfig((64, 32, 1))] + cfgs[40:]  # 2048 threads: FootprintError
+        try:
+            kept, order, rec = gvo.rank_sweep_sharded(fam, cfgs, m, skip_invalid=True, group=group)
+            out_q.put((rank, [c.key for c in kept], order, rec))
+        except Exception as exc:  # noqa: BLE001
+            out_q.put((rank, "raised", type(exc).__name__, str(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_world(world, case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_engine_worker, args=(r, world, port, q, case)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["world2", "subgroup"])
+def test_sharded_engine_equals_single_gpu_rank_sweep(case):
+    """rank_sweep_sharded through the real engine on two ranks (gloo; both
+    on the box's one GPU) gives rank_sweep's kept configs, order and
+    records on every rank — including a subgroup of a three-rank world."""
+    from paper_2107_01143_b200 import gvo
+
+    res = _run_world(3 if case == "subgroup" else 2, case)
+    m = gvo.b200_preset()
+    fam = gvo.KernelFamily("stencil", (64, 64, 64), radius=2)
+    cfgs = list(gvo.enumerate_sweep(64, foldings=("none", "2y", "2z"))) + list(gvo.enumerate_sweep(512))
+    rows = gvo.rank_sweep(fam, cfgs, m, skip_invalid=True)
+    want_keys = [c.key for c in rows.configs]
+    members = [r for r in res if r[1] is not None]
+    assert len(members) == 2
+    for _, keys, order, rec in members:
+        assert keys == want_keys
+        np.testing.assert_array_equal(order, rows.order)
+        np.testing.assert_array_equal(rec, rows.records)
+
+
+@pytest.mark.gpu
+def test_sharded_engine_every_rank_raises_the_reference_error():
+    """An evaluation error on one rank's shard raises the reference's
+    exception on every rank (no rank left waiting in the collective)."""
+    res = _run_world(2, "error")
+    for r in res:
+        assert r[1] == "raised" and r[2] == "FootprintError", r
+        assert "exceeds machine limit" in r[3]
+
+
+@pytest.mark.gpu
+def test_torchrun_bench_two_ranks_ranks_like_one(tmp_path):
+    """bench.py under torchrun with two ranks (gloo on the one test GPU):
+    cost-dealt shards, all-gather, gvo_rank_gathered — the global ranking
+    equals the single-rank one."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, GVO_BENCH_BACKEND="gloo")
+    common = ["--workload", "C4", "--steps", "1", "--warmup", "1", "--no-cpu"]
+    one = subprocess.run([sys.executable, str(root / "bench.py"), *common, "--dump-order", str(tmp_path / "o1.npy")],
+                         capture_output=True, text=True, timeout=900, cwd=root, env=env)
+    assert one.returncode == 0, one.stderr[-3000:]
+    two = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(root / "bench.py"),
+                          *common, "--gpus", "2", "--dump-order", str(tmp_path / "o2.npy")],
+                         capture_output=True, text=True, timeout=900, cwd=root, env=env)
+    assert two.returncode == 0, two.stderr[-3000:]
+    line = json.loads([ln for ln in two.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong" and line["e2e"]["value"] > 0
+    np.testing.assert_array_equal(np.load(tmp_path / "o1.npy"), np.load(tmp_path / "o2.npy"))

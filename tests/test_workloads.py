@@ -136,3 +136,33 @@ def test_full_sweep_ranking_identical_to_reference(name):
     lim = [gvo.perf.LIMITER_ORDER[int(x)] for x in res.records[:, -2]]
     assert lim == g["limiter"]
     assert list(map(int, order)) == g["order"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_seeded_subset_records_and_ranking_vs_reference(name):
+    """512 seeded configurations of each large space: every
+    record column bit-identical to the reference's and the subset ranked in
+    the reference's order (tests/golden/subsets.json)."""
+    g = load("subsets")
+    s = g["spaces"][name]
+    cols = g["columns"]
+    ents = [{"template": s["templates"][t], "machine": mm, "block": [bx, by, bz]} for t, mm, bx, by, bz in s["cfg"]]
+    assert all(isinstance(r, list) for r in s["records"])
+    sp = W.space_from_entries(ents, _machines(name))
+    res, order = W.evaluate_space(sp)
+    lim_col = cols.index("limiter")
+    bad = []
+    for i, want in enumerate(s["records"]):
+        for c, (col, w) in enumerate(zip(cols, want)):
+            got = res.records[i, c]
+            if c == lim_col:
+                ok = gvo.perf.LIMITER_ORDER[int(got)] == w
+            elif w is None:
+                ok = np.isnan(got)
+            else:
+                ok = float(got).hex() == w
+            if not ok:
+                bad.append((sp.key(i), col, float(got).hex(), w))
+    assert not bad, bad[:5]
+    assert list(map(int, order)) == s["order"]
