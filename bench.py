@@ -346,6 +346,8 @@ def run_device(args, rank, world):
         if world == 1 and not np.array_equal(order_pin, final_order):
             raise AssertionError("e2e ranking differs from the device-timed ranking")
 
+    api = api_leg(ctx, smp) if world == 1 and not args.no_e2e else None
+
     if args.dump_order and rank == 0:
         np.save(args.dump_order, final_order)
     if rank != 0:
@@ -374,6 +376,7 @@ def run_device(args, rank, world):
         "gpu_launches": int(sum(kcnt[i] for i in range(5))),
         "launches_per_step": {k: v / max(1, args.steps) for k, v in launches.items()},
         "kernel_ms_per_step": kernel_ms,
+        "e2e_api": api,
         "rank_ms": ms_all if world > 1 else None,
         "roofline": roof,
         "cpu_baseline": cpu,
@@ -382,6 +385,44 @@ def run_device(args, rank, world):
         "build_id": bid,
     }
     print(json.dumps(line), flush=True)
+
+
+def api_leg(ctx, smp, reps: int = 5):
+    """The drop-in Python API (gvo.rank_sweep, reference perf.py:98-132)
+    against the one-call C ABI (gvo_sweep_host) on the same sweep: the
+    reference's own KernelFamily("stencil", 640^3, r=4) over every
+    power-of-two block <= 1024 threads (C2, skip_invalid).  Host-side
+    validation, batch construction, evaluation, ranking and row access
+    (len / first row) are inside the timed region."""
+    from paper_2107_01143_b200 import _native, gvo
+
+    m = gvo.b200_preset()
+    fam = gvo.KernelFamily("stencil", (640, 640, 640), radius=4)
+    cfgs = [c for t in (1 << i for i in range(11)) for c in gvo.enumerate_sweep(t)]
+    rows = gvo.rank_sweep(fam, cfgs, m, skip_invalid=True)  # warm: templates registered
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        rows = gvo.rank_sweep(fam, cfgs, m, skip_invalid=True)
+        _ = rows[0].prediction.glups
+    api_s = (time.perf_counter() - t0) / reps
+    n = len(rows)
+    plan = gvo.perf.SweepPlan(fam, cfgs, m, skip_invalid=True)
+    ca = plan.config_array()
+    ctx.sync_registries()
+    F = ctx.max_fields
+    S, W = _native.effective_sampling(5, 2)
+    counts = np.zeros((n, _native.counts_stride(F, S, W)), dtype=np.int64)
+    rec = np.zeros((n, _native.RECORD_LEN))
+    order = np.zeros(n, dtype=np.int64)
+    C = _native.C
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        ctx.check(_native.lib().gvo_sweep_host(ctx.h, _native._ptr(ca), n, C.byref(smp), F, _native._ptr(counts),
+                                               None, _native._ptr(rec), _native._ptr(order)))
+    abi_s = (time.perf_counter() - t0) / reps
+    assert np.array_equal(order, rows.order)
+    return {"workload": f"C2 sweep through gvo.rank_sweep ({len(cfgs)} configs, {n} valid)",
+            "value": n / api_s, "unit": "configs/s", "c_abi_value": n / abi_s, "fraction_of_c_abi": abi_s / api_s}
 
 
 def _gather_np(a: np.ndarray, world: int):

@@ -4,6 +4,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <nvtx3/nvToolsExt.h>
 #include "gvo_kernels.h"
 #include "gvo_bytecode.cuh"
 
@@ -127,14 +128,22 @@ struct gvo_ctx {
   int64_t unit_items = 0;
 };
 
-// kernel ids for timing: 0 setup, 1 warp, 2 sets, 3 finish, 4 rank
+// kernel ids for timing: 0 setup, 1 warp, 2 sets, 3 finish, 4 rank.  Every
+// pipeline stage is also an NVTX range ("gvo.<stage>", nested in "gvo.batch"),
+// so ncu --nvtx / any NVTX tool can attribute launches to stages.
+struct NvtxRange {  // scoped: popped on every return path
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+static const char* const kStageName[5] = {"gvo.setup", "gvo.warp", "gvo.sets", "gvo.finish", "gvo.rank"};
 static void tmark_begin(gvo_ctx* ctx, int id, cudaStream_t st, cudaEvent_t* b) {
+  nvtxRangePushA(kStageName[id]);
   if (!ctx->timing) return;
   cudaEventCreate(b);
   cudaEventRecord(*b, st);
-  (void)id;
 }
 static void tmark_end(gvo_ctx* ctx, int id, cudaStream_t st, cudaEvent_t b) {
+  nvtxRangePop();
   if (!ctx->timing) return;
   cudaEvent_t e;
   cudaEventCreate(&e);
@@ -388,6 +397,7 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     const int64_t nb = std::min(ctx->batch, n - b0);
     int rc = ensure_work(ctx, nb);
     if (rc) return rc;
+    NvtxRange batch_range("gvo.batch");
     const gvo_config* cf = d_cfgs + b0;
     int64_t* cnt = d_counts + b0 * stride;
     CK(cudaMemsetAsync(cnt, 0, (size_t)nb * stride * 8, st));

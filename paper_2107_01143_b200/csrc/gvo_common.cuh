@@ -172,6 +172,63 @@ __host__ __device__ inline int run_boxes(int64_t s, int64_t cnt, const int64_t g
   return nb;
 }
 
+// The bi-th box of run_boxes (false when the run has fewer boxes) and the
+// box count, without a box array (no local-memory array in the callers).
+__host__ __device__ __forceinline__ bool run_box_at(int64_t s, int64_t cnt, const int64_t g[3], int bi, Box* out) {
+  const int64_t L = g[0], P = g[0] * g[1];
+  const int64_t e = s + cnt;
+  int64_t cur = s;
+  for (int k = 0; cur < e; ++k) {
+    Box b;
+    if (cur % L != 0 || e - cur < L) {
+      int64_t end = (cur / L + 1) * L;
+      if (end > e) end = e;
+      b.lo[0] = cur % L; b.n[0] = end - cur;
+      b.lo[1] = (cur / L) % g[1]; b.n[1] = 1;
+      b.lo[2] = cur / P; b.n[2] = 1;
+      cur = end;
+    } else if (cur % P != 0 || e - cur < P) {
+      int64_t y0 = (cur / L) % g[1];
+      int64_t rows = (e - cur) / L;
+      if (rows > g[1] - y0) rows = g[1] - y0;
+      b.lo[0] = 0; b.n[0] = L;
+      b.lo[1] = y0; b.n[1] = rows;
+      b.lo[2] = cur / P; b.n[2] = 1;
+      cur += rows * L;
+    } else {
+      int64_t layers = (e - cur) / P;
+      b.lo[0] = 0; b.n[0] = L;
+      b.lo[1] = 0; b.n[1] = g[1];
+      b.lo[2] = cur / P; b.n[2] = layers;
+      cur += layers * P;
+    }
+    if (k == bi) { *out = b; return true; }
+  }
+  return false;
+}
+
+__host__ __device__ inline int run_box_count(int64_t s, int64_t cnt, const int64_t g[3]) {
+  const int64_t L = g[0], P = g[0] * g[1];
+  const int64_t e = s + cnt;
+  int64_t cur = s;
+  int nb = 0;
+  while (cur < e) {
+    if (cur % L != 0 || e - cur < L) {
+      int64_t end = (cur / L + 1) * L;
+      cur = end > e ? e : end;
+    } else if (cur % P != 0 || e - cur < P) {
+      int64_t rows = (e - cur) / L;
+      const int64_t y0 = (cur / L) % g[1];
+      if (rows > g[1] - y0) rows = g[1] - y0;
+      cur += rows * L;
+    } else {
+      cur += ((e - cur) / P) * P;
+    }
+    ++nb;
+  }
+  return nb;
+}
+
 // Coordinate bounds of a run of blocks (min/max of each block coordinate),
 // as the reference's _GroupEval computes them (footprint.py:262-269).
 __host__ __device__ inline void run_bid_bounds(int64_t s, int64_t cnt, const int64_t g[3],

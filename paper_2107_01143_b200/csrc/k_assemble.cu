@@ -66,22 +66,43 @@ void launch_predict(const gvo_machine* d_machines, const int32_t* d_mid, const d
   k_predict<<<(unsigned)((n + 63) / 64), 64, 0, st>>>(d_machines, d_mid, dd, ld, cyc, fl, n, out);
 }
 
+// Python's built-in sum() over floats (CPython >= 3.12, bltinmodule.c
+// builtin_sum_impl): the int start 0 plus the first item is exact (0 + x),
+// every further item is added with Neumaier's compensation, and the
+// compensation is added at the end when it is nonzero and finite.  The
+// reference sums per-field volumes with sum() (volumes.py:307-309, 332,
+// 386, 401-404, 416); plain left-to-right addition differs in the last bit
+// whenever the sum is inexact.
+struct PySum {
+  double s = 0.0, c = 0.0;
+  bool any = false;
+  __device__ __forceinline__ void add(double x) {
+    if (!any) { s = 0.0 + x; any = true; return; }
+    const double t = s + x;
+    if (fabs(s) >= fabs(x)) c += (s - t) + x;
+    else c += (x - t) + s;
+    s = t;
+  }
+  __device__ __forceinline__ double value() const { return (c != 0.0 && isfinite(c)) ? s + c : s; }
+};
+
 // _assemble + _totals for F fields; writes (up, comp, red, cap, down)
 __device__ inline void assemble_level(int F, const double* comp_f, const double* up_f,
                                       const double* basis_f, double ratio, double* down_f,
                                       double out[5]) {
-  double sc = 0.0, sr = 0.0, sk = 0.0;
+  PySum Sc, Sr, Sk;
   for (int f = 0; f < F; ++f) {
     const double up = up_f[f];
     const double c = pmin(comp_f[f], up);
     const double r = pmax(0.0, up - c);
     const double k = pmin(pmax(ratio * basis_f[f], 0.0), r);
     down_f[f] = c + k;
-    sc = sc + c;
-    sr = sr + r;
-    sk = sk + k;
+    Sc.add(c);
+    Sr.add(r);
+    Sk.add(k);
   }
-  const double k = pmin(sk, sr);
+  const double sc = Sc.value(), sr = Sr.value();
+  const double k = pmin(Sk.value(), sr);
   out[0] = sc + sr;
   out[1] = sc;
   out[2] = sr;
@@ -114,9 +135,9 @@ __device__ void assemble_one(const gvo_machine& m, int F, const double* st, int6
   double lv[5], sv[5], dl[5], ds[5];
 
   // ---- L2 -> L1 (volumes.py:313-351)
-  double alloc_sum = 0.0;
-  for (int f = 0; f < F; ++f) alloc_sum = alloc_sum + load_alloc[f];
-  const double alloc = alloc_sum * lups_per_block;
+  PySum alloc_sum;
+  for (int f = 0; f < F; ++f) alloc_sum.add(load_alloc[f]);
+  const double alloc = alloc_sum.value() * lups_per_block;
   const double oversub1 = alloc / (double)m.l1_capacity_bytes;
   const double ratio1 = gompertz(m.fit[0], oversub1);
   for (int f = 0; f < F; ++f) basis[f] = pmax(0.0, load_up[f] - load_comp[f]);
@@ -140,10 +161,10 @@ __device__ void assemble_one(const gvo_machine& m, int F, const double* st, int6
   bool has_cov = false;
   double coverage = 0.0, om_ratio = 0.0;
   if (has_pred && prev_total > 0.0) {
-    double su = 0.0, so = 0.0;
-    for (int f = 0; f < F; ++f) su = su + w_load_unique[f];
-    for (int f = 0; f < F; ++f) so = so + w_load_overlap[f];
-    const double net_new = su - so;
+    PySum su, so;
+    for (int f = 0; f < F; ++f) su.add(w_load_unique[f]);
+    for (int f = 0; f < F; ++f) so.add(w_load_overlap[f]);
+    const double net_new = su.value() - so.value();
     coverage = ((double)m.l2_capacity_bytes - net_new) / prev_total;
     has_cov = true;
     om_ratio = gompertz(m.fit[3], -coverage);
@@ -151,25 +172,27 @@ __device__ void assemble_one(const gvo_machine& m, int F, const double* st, int6
     for (int f = 0; f < F; ++f) overlap[f] = 0.0;
   }
   double comp_raw[kMaxFields], red_basis[kMaxFields];
-  double su = 0.0, so = 0.0, sb = 0.0;
+  PySum su, so, sb;
   for (int f = 0; f < F; ++f) {
     comp_raw[f] = (unique[f] - overlap[f]) + om_ratio * overlap[f];
     red_basis[f] = pmax(0.0, d_l2l1_load[f] - unique[f]);
   }
   const double ratio2 = gompertz(m.fit[1], oversub2);
   assemble_level(F, comp_raw, d_l2l1_load, red_basis, ratio2, d_dram_load, dl);
-  for (int f = 0; f < F; ++f) su = su + unique[f];
-  for (int f = 0; f < F; ++f) so = so + overlap[f];
-  for (int f = 0; f < F; ++f) sb = sb + red_basis[f];
-  const double wave_unique = su, v_overlap = so, overmiss = om_ratio * so, v_red_l2 = sb;
+  for (int f = 0; f < F; ++f) su.add(unique[f]);
+  for (int f = 0; f < F; ++f) so.add(overlap[f]);
+  for (int f = 0; f < F; ++f) sb.add(red_basis[f]);
+  const double wave_unique = su.value(), v_overlap = so.value(), overmiss = om_ratio * so.value(),
+               v_red_l2 = sb.value();
 
   double* s_unique = tmp_a;  // unique/overlap no longer needed
   for (int f = 0; f < F; ++f) s_unique[f] = w_store_unique[f] / wave_lups;
   for (int f = 0; f < F; ++f) basis[f] = pmax(0.0, d_l2l1_store[f] - s_unique[f]);
   const double ratio3 = gompertz(m.fit[2], oversub2);
   assemble_level(F, s_unique, d_l2l1_store, basis, ratio3, d_dram_store, ds);
-  double s_wave_unique = 0.0;
-  for (int f = 0; f < F; ++f) s_wave_unique = s_wave_unique + s_unique[f];
+  PySum sw;
+  for (int f = 0; f < F; ++f) sw.add(s_unique[f]);
+  const double s_wave_unique = sw.value();
 
   // ---- predict (perf.py:45-67)
   double t[4];

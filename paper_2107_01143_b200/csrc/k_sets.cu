@@ -111,54 +111,99 @@ struct UnitSh {
 };
 
 // ------------------------------------------------------------------ lattice
-struct Lat {
+// A lattice of addresses base + sum_d st_d * k_d (k_d < ex_d) with an inner
+// granule-contiguous byte span.  Two register-resident forms, so that no
+// lattice ever lives in local memory (a per-thread array indexed by a
+// runtime dimension would, and under a 2x110 KB shared-memory carve-out the
+// L1 cannot hold the stacks of 640 threads: the previous per-thread form
+// moved ~190 MB of stack through DRAM per C2 launch):
+//  * WLat — held by a whole warp, lane d < nd holding dimension d; every
+//    step (normalise, split, emit) is warp-cooperative with shuffles.  Used
+//    for the box lattices and the translate covers (a handful of lattices
+//    per task, emitted one after another by the warp);
+//  * Lat4 — per lane, at most kSegDims dimensions, every loop unrolled with
+//    compile-time indices.  Used by the segment cover, whose lanes emit one
+//    segment box each.
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kSegDims = 4;
+
+struct WLat {
+  int64_t base;   // warp-uniform
+  uint64_t span;  // warp-uniform
+  int nd;         // warp-uniform
+  uint64_t st;    // lane d < nd: stride of dimension d (0 elsewhere)
+  int64_t ex;     // lane d < nd: extent of dimension d (1 elsewhere)
+};
+
+struct Lat4 {
   int64_t base;
   uint64_t span;
   int nd;
-  uint64_t st[kMaxDims];
-  int64_t ex[kMaxDims];
+  uint64_t st[kSegDims];
+  int64_t ex[kSegDims];
 };
 
-__device__ inline void sort_dims(Lat& L) {
-  for (int i = 1; i < L.nd; ++i) {
-    uint64_t s = L.st[i];
-    int64_t e = L.ex[i];
-    int k = i - 1;
-    while (k >= 0 && L.st[k] > s) { L.st[k + 1] = L.st[k]; L.ex[k + 1] = L.ex[k]; --k; }
-    L.st[k + 1] = s;
-    L.ex[k + 1] = e;
-  }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
 }
 
-// merge dims whose union is again an arithmetic progression, then fold the
-// leading dims whose point gaps stay <= g into the granule-contiguous span.
-__device__ inline void normalize(Lat& L, int64_t g) {
-  sort_dims(L);
-  int m = 0;
-  for (int i = 0; i < L.nd; ++i) {
-    if (L.ex[i] <= 1 || L.st[i] == 0) continue;
-    if (m > 0) {
-      const uint64_t sc = L.st[m - 1];
-      const int64_t sn = L.ex[m - 1];
-      if (L.st[i] % sc == 0 && L.st[i] / sc <= (uint64_t)sn) {
-        L.ex[m - 1] = sn + (int64_t)(L.st[i] / sc) * (L.ex[i] - 1);
+// Merge dims whose union is again an arithmetic progression (sorted by
+// stride, st_j % st_i == 0 && st_j / st_i <= ex_i), then fold the leading
+// dims whose point gaps stay <= g into the granule-contiguous span.
+// Warp-cooperative; dims with ex <= 1 or st == 0 are dropped.
+__device__ __forceinline__ void wl_normalize(WLat& L, int64_t g) {
+  const int lane = threadIdx.x & 31;
+  const bool keep = lane < L.nd && L.ex > 1 && L.st != 0;
+  const unsigned kmask = __ballot_sync(kFull, keep);
+  // rank among kept dims by (stride, dim)
+  int r = 0;
+  for (int j = 0; j < L.nd; ++j) {
+    const uint64_t sj = __shfl_sync(kFull, L.st, j);
+    r += ((kmask >> j) & 1u) && (sj < L.st || (sj == L.st && j < lane));
+  }
+  uint64_t s2 = 0;
+  int64_t e2 = 1;
+  for (int j = 0; j < L.nd; ++j) {
+    const int rj = __shfl_sync(kFull, r, j);
+    const uint64_t sj = __shfl_sync(kFull, L.st, j);
+    const int64_t ej = __shfl_sync(kFull, L.ex, j);
+    if (((kmask >> j) & 1u) && rj == lane) { s2 = sj; e2 = ej; }
+  }
+  const int m = __popc(kmask);
+  uint64_t so = 0;
+  int64_t eo = 1;
+  int o = 0;
+  for (int i = 0; i < m; ++i) {
+    const uint64_t si = __shfl_sync(kFull, s2, i);
+    const int64_t ei = __shfl_sync(kFull, e2, i);
+    if (o > 0) {
+      const uint64_t sc = __shfl_sync(kFull, so, o - 1);
+      const int64_t sn = __shfl_sync(kFull, eo, o - 1);
+      if (si % sc == 0 && si / sc <= (uint64_t)sn) {
+        if (lane == o - 1) eo = sn + (int64_t)(si / sc) * (ei - 1);
         continue;
       }
     }
-    L.st[m] = L.st[i];
-    L.ex[m] = L.ex[i];
-    ++m;
+    if (lane == o) { so = si; eo = ei; }
+    ++o;
   }
-  L.nd = m;
+  uint64_t span = L.span;
   int k = 0;
-  while (k < L.nd && (unsigned __int128)L.st[k] <= (unsigned __int128)L.span + (uint64_t)g) {
-    L.span += L.st[k] * (uint64_t)(L.ex[k] - 1);
+  while (k < o) {
+    const uint64_t sk = __shfl_sync(kFull, so, k);
+    const int64_t ek = __shfl_sync(kFull, eo, k);
+    if ((unsigned __int128)sk > (unsigned __int128)span + (uint64_t)g) break;
+    span += sk * (uint64_t)(ek - 1);
     ++k;
   }
-  if (k) {
-    for (int i = k; i < L.nd; ++i) { L.st[i - k] = L.st[i]; L.ex[i - k] = L.ex[i]; }
-    L.nd -= k;
-  }
+  const uint64_t s3 = __shfl_sync(kFull, so, (lane + k) & 31);
+  const int64_t e3 = __shfl_sync(kFull, eo, (lane + k) & 31);
+  L.nd = o - k;
+  L.span = span;
+  L.st = lane < L.nd ? s3 : 0;
+  L.ex = lane < L.nd ? e3 : 1;
 }
 
 __device__ inline bool contains(const int64_t* P, int n, int64_t v) {
@@ -181,60 +226,230 @@ struct RunSink {
   int* has_pattern = nullptr;  // set when a pattern run is emitted (bitmap tier only)
 };
 
-__device__ inline void emit_normalized(const RunSink& S, const Lat& L, int tag, const Granule& G);
+// Emit normalised lattices that share their dims (held by the warp) and
+// differ in their base: one run per active lane (`act`, this lane's base
+// `b`).  Warp-cooperative: one slot reservation, the dims written by the
+// lanes that hold them.
+__device__ __forceinline__ void wl_emit_normalized(const RunSink& S, const WLat& L, int64_t b, bool act, int tag,
+                                                const Granule& G) {
+  const int lane = threadIdx.x & 31;
+  int64_t count = 1;
+  uint64_t ext_span = L.span;
+  bool over = false;
+  bool mono = true;
+  unsigned __int128 reach = (unsigned __int128)L.span;
+  for (int d = 0; d < L.nd; ++d) {
+    const uint64_t sd = __shfl_sync(kFull, L.st, d);
+    const int64_t ed = __shfl_sync(kFull, L.ex, d);
+    if (count > (int64_t(1) << 40) / ed) over = true;
+    else count *= ed;
+    ext_span += sd * (uint64_t)(ed - 1);
+    if (d > 0 && (unsigned __int128)sd <= reach) mono = false;
+    reach += (unsigned __int128)sd * (uint64_t)(ed - 1);
+  }
+  const unsigned am = __ballot_sync(kFull, act);
+  if (!am) return;
+  if (over) {
+    if (lane == 0) atomicExch(S.status, GVO_ERR_CAPACITY);
+    return;
+  }
+  const int64_t len = (int64_t)(L.span / (uint64_t)G.g) + 2;
+  const int64_t pieces = (len + kPiece - 1) / kPiece;
+  mono = mono && pieces == 1;
+  int slot0 = 0;
+  if (lane == 0) slot0 = atomicAdd(S.n_runs, __popc(am));
+  slot0 = __shfl_sync(kFull, slot0, 0);
+  if (slot0 + __popc(am) > S.cap) {
+    if (lane == 0) atomicExch(S.status, GVO_ERR_CAPACITY);
+    return;
+  }
+  if (act) {
+    Run* r = S.runs + slot0 + __popc(am & lanemask_lt());
+    r->base = b;
+    r->span = L.span;
+    r->nd = L.nd;
+    r->tag = tag;
+    r->kind = 0;
+    r->access = -1;
+    r->pieces = pieces;
+    r->count = count * pieces;
+    r->mono = mono ? 1 : 0;
+    r->run_start = r->run_count = 0;
+  }
+  // dims: lanes d < kMaxDims write dimension d of every emitted run
+  for (int q = 0; q < __popc(am); ++q) {
+    Run* r = S.runs + slot0 + q;
+    if (lane < kMaxDims) {
+      r->stride[lane] = lane < L.nd ? (int64_t)L.st : 0;
+      r->ext[lane] = lane < L.nd ? L.ex : 1;
+    }
+  }
+  // key bounds: warp min/max, one atomic each
+  long long lo = act ? (long long)G.of(b) : LLONG_MAX;
+  long long hi = act ? (long long)G.of((int64_t)((uint64_t)b + ext_span)) : LLONG_MIN;
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(kFull, lo, o));
+    hi = max(hi, __shfl_xor_sync(kFull, hi, o));
+  }
+  if (lane == 0) {
+    atomicMin((long long*)S.key_lo, lo);
+    atomicMax((long long*)S.key_hi, hi);
+  }
+}
 
 // Normalise, then split off the dimensions that interleave with faster
 // ones (a stride not beyond the reach of the kept faster dimensions, e.g. a
 // translate pair 192 B apart on a 120 B-stride row): the sub-lattices over
 // the remaining dimensions are monotone, so key ranges can bisect them
-// instead of scanning.  Splitting is bounded (<= 64 sub-lattices); beyond
-// that the lattice is emitted as one non-monotone run.
-__device__ inline void emit_lattice(const RunSink& S, Lat L, int tag, const Granule& G) {
-  normalize(L, G.g);
-  int split[kMaxDims];
-  int ns = 0;
+// instead of scanning.  Splitting is bounded (<= 64 sub-lattices, emitted
+// by the lanes in parallel); beyond that the lattice is emitted as one
+// non-monotone run.  Warp-cooperative.
+__device__ __forceinline__ void wl_emit_lattice(const RunSink& S, WLat L, int tag, const Granule& G) {
+  const int lane = threadIdx.x & 31;
+  wl_normalize(L, G.g);
+  unsigned smask = 0;
   int64_t combos = 1;
   {
     unsigned __int128 reach = (unsigned __int128)L.span;
     for (int d = 0; d < L.nd; ++d) {
-      if (d > 0 && (unsigned __int128)L.st[d] <= reach) {
-        split[ns++] = d;
-        combos *= L.ex[d];
+      const uint64_t sd = __shfl_sync(kFull, L.st, d);
+      const int64_t ed = __shfl_sync(kFull, L.ex, d);
+      if (d > 0 && (unsigned __int128)sd <= reach) {
+        smask |= 1u << d;
+        combos = combos > 64 || ed > 64 ? 65 : combos * ed;
       } else {
-        reach += (unsigned __int128)L.st[d] * (uint64_t)(L.ex[d] - 1);
+        reach += (unsigned __int128)sd * (uint64_t)(ed - 1);
       }
     }
   }
-  if (ns == 0 || combos > 64) { emit_normalized(S, L, tag, G); return; }
-  Lat K;
-  K.span = L.span;
-  K.nd = 0;
-  for (int d = 0, q = 0; d < L.nd; ++d) {
-    if (q < ns && split[q] == d) { ++q; continue; }
-    K.st[K.nd] = L.st[d];
-    K.ex[K.nd] = L.ex[d];
-    ++K.nd;
+  if (smask == 0 || combos > 64) {
+    wl_emit_normalized(S, L, L.base, lane == 0, tag, G);
+    return;
   }
-  for (int64_t m = 0; m < combos; ++m) {
+  // K: the kept dims, compacted
+  const unsigned ndmask = L.nd >= 32 ? kFull : ((1u << L.nd) - 1u);
+  const unsigned kept = ndmask & ~smask;
+  WLat K;
+  K.span = L.span;
+  K.nd = __popc(kept);
+  K.base = L.base;
+  K.st = 0;
+  K.ex = 1;
+  for (int d = 0; d < L.nd; ++d) {
+    const uint64_t sd = __shfl_sync(kFull, L.st, d);
+    const int64_t ed = __shfl_sync(kFull, L.ex, d);
+    if (((kept >> d) & 1u) && __popc(kept & ((1u << d) - 1u)) == lane) { K.st = sd; K.ex = ed; }
+  }
+  // sub-lattice m: base + sum over split dims (ascending) of st_d * digit_d(m)
+  for (int m0 = 0; m0 < combos; m0 += 32) {
+    const int m = m0 + lane;
     int64_t r = m;
     uint64_t b = (uint64_t)L.base;
-    for (int q = 0; q < ns; ++q) {
-      const int d = split[q];
-      b += L.st[d] * (uint64_t)(r % L.ex[d]);
-      r /= L.ex[d];
+    for (int d = 0; d < L.nd; ++d) {
+      const uint64_t sd = __shfl_sync(kFull, L.st, d);
+      const int64_t ed = __shfl_sync(kFull, L.ex, d);
+      if ((smask >> d) & 1u) {
+        b += sd * (uint64_t)(r % ed);
+        r /= ed;
+      }
     }
-    K.base = (int64_t)b;
-    emit_normalized(S, K, tag, G);
+    wl_emit_normalized(S, K, (int64_t)b, m < combos, tag, G);
   }
 }
 
-__device__ inline void emit_normalized(const RunSink& S, const Lat& L, int tag, const Granule& G) {
+// ---- per-lane lattices of at most kSegDims dims (segment boxes)
+// every loop over dims has compile-time bounds and indices: registers only
+__device__ __forceinline__ void l4_cswap(uint64_t& sa, int64_t& ea, uint64_t& sb, int64_t& eb) {
+  if (sb < sa) {
+    const uint64_t ts = sa; sa = sb; sb = ts;
+    const int64_t te = ea; ea = eb; eb = te;
+  }
+}
+
+__device__ __forceinline__ void l4_normalize(Lat4& L, int64_t g) {
+  uint64_t s[kSegDims];
+  int64_t e[kSegDims];
+#pragma unroll
+  for (int d = 0; d < kSegDims; ++d) {
+    const bool ok = d < L.nd && L.ex[d] > 1 && L.st[d] != 0;
+    s[d] = ok ? L.st[d] : ~0ull;  // dropped dims sort last
+    e[d] = ok ? L.ex[d] : 1;
+  }
+  l4_cswap(s[0], e[0], s[1], e[1]);
+  l4_cswap(s[2], e[2], s[3], e[3]);
+  l4_cswap(s[0], e[0], s[2], e[2]);
+  l4_cswap(s[1], e[1], s[3], e[3]);
+  l4_cswap(s[1], e[1], s[2], e[2]);
+  uint64_t os[kSegDims];
+  int64_t oe[kSegDims];
+#pragma unroll
+  for (int d = 0; d < kSegDims; ++d) { os[d] = 0; oe[d] = 1; }
+  int m = 0;
+  uint64_t sc = 0;
+  int64_t sn = 1;
+  bool have = false;
+#pragma unroll
+  for (int i = 0; i < kSegDims; ++i) {
+    if (s[i] == ~0ull) continue;
+    if (have && s[i] % sc == 0 && s[i] / sc <= (uint64_t)sn) {
+      sn = sn + (int64_t)(s[i] / sc) * (e[i] - 1);
+      continue;
+    }
+    if (have) {
+#pragma unroll
+      for (int j = 0; j < kSegDims; ++j)
+        if (j == m) { os[j] = sc; oe[j] = sn; }
+      ++m;
+    }
+    sc = s[i];
+    sn = e[i];
+    have = true;
+  }
+  if (have) {
+#pragma unroll
+    for (int j = 0; j < kSegDims; ++j)
+      if (j == m) { os[j] = sc; oe[j] = sn; }
+    ++m;
+  }
+  uint64_t span = L.span;
+  int k = 0;
+  bool stop = false;
+#pragma unroll
+  for (int j = 0; j < kSegDims; ++j) {
+    if (!stop && j < m && (unsigned __int128)os[j] <= (unsigned __int128)span + (uint64_t)g) {
+      span += os[j] * (uint64_t)(oe[j] - 1);
+      k = j + 1;
+    } else {
+      stop = true;
+    }
+  }
+  L.span = span;
+  L.nd = m - k;
+#pragma unroll
+  for (int j = 0; j < kSegDims; ++j) {
+    uint64_t sv = 0;
+    int64_t ev = 1;
+#pragma unroll
+    for (int q = 0; q < kSegDims; ++q)
+      if (q == j + k) { sv = os[q]; ev = oe[q]; }
+    L.st[j] = j < L.nd ? sv : 0;
+    L.ex[j] = j < L.nd ? ev : 1;
+  }
+}
+
+__device__ __forceinline__ void l4_emit_normalized(const RunSink& S, const Lat4& L, int tag, const Granule& G) {
   int64_t count = 1;
   uint64_t ext_span = L.span;
-  for (int d = 0; d < L.nd; ++d) {
+  bool mono = true;
+  unsigned __int128 reach = (unsigned __int128)L.span;
+#pragma unroll
+  for (int d = 0; d < kSegDims; ++d) {
+    if (d >= L.nd) continue;
     if (count > (int64_t(1) << 40) / L.ex[d]) { atomicExch(S.status, GVO_ERR_CAPACITY); return; }
     count *= L.ex[d];
     ext_span += L.st[d] * (uint64_t)(L.ex[d] - 1);
+    if (d > 0 && (unsigned __int128)L.st[d] <= reach) mono = false;
+    reach += (unsigned __int128)L.st[d] * (uint64_t)(L.ex[d] - 1);
   }
   const int64_t len = (int64_t)(L.span / (uint64_t)G.g) + 2;
   const int64_t pieces = (len + kPiece - 1) / kPiece;
@@ -244,29 +459,66 @@ __device__ inline void emit_normalized(const RunSink& S, const Lat& L, int tag, 
   r->base = L.base;
   r->span = L.span;
   r->nd = L.nd;
+#pragma unroll
   for (int d = 0; d < kMaxDims; ++d) {
-    r->stride[d] = d < L.nd ? (int64_t)L.st[d] : 0;
-    r->ext[d] = d < L.nd ? L.ex[d] : 1;
+    r->stride[d] = d < kSegDims && d < L.nd ? (int64_t)L.st[d < kSegDims ? d : 0] : 0;
+    r->ext[d] = d < kSegDims && d < L.nd ? L.ex[d < kSegDims ? d : 0] : 1;
   }
   r->tag = tag;
   r->kind = 0;
   r->access = -1;
   r->pieces = pieces;
   r->count = count * pieces;
-  // monotone: with dim 0 fastest, every dim's stride exceeds the span plus
-  // the reach of all faster dims -> bases and interval ends increase with k
-  {
-    bool mono = pieces == 1;
-    unsigned __int128 reach = (unsigned __int128)L.span;
-    for (int d = 0; d < L.nd && mono; ++d) {
-      if (d > 0 && (unsigned __int128)L.st[d] <= reach) mono = false;
-      reach += (unsigned __int128)L.st[d] * (uint64_t)(L.ex[d] - 1);
-    }
-    r->mono = mono ? 1 : 0;
-  }
+  r->mono = mono && pieces == 1 ? 1 : 0;
   r->run_start = r->run_count = 0;
   atomicMin((long long*)S.key_lo, (long long)G.of(L.base));
   atomicMax((long long*)S.key_hi, (long long)G.of((int64_t)((uint64_t)L.base + ext_span)));
+}
+
+// per-lane twin of wl_emit_lattice
+__device__ __forceinline__ void l4_emit_lattice(const RunSink& S, Lat4 L, int tag, const Granule& G) {
+  l4_normalize(L, G.g);
+  unsigned smask = 0;
+  int64_t combos = 1;
+  {
+    unsigned __int128 reach = (unsigned __int128)L.span;
+#pragma unroll
+    for (int d = 0; d < kSegDims; ++d) {
+      if (d >= L.nd) continue;
+      if (d > 0 && (unsigned __int128)L.st[d] <= reach) {
+        smask |= 1u << d;
+        combos = combos > 64 || L.ex[d] > 64 ? 65 : combos * L.ex[d];
+      } else {
+        reach += (unsigned __int128)L.st[d] * (uint64_t)(L.ex[d] - 1);
+      }
+    }
+  }
+  if (smask == 0 || combos > 64) { l4_emit_normalized(S, L, tag, G); return; }
+  Lat4 K;
+  K.span = L.span;
+  K.nd = 0;
+#pragma unroll
+  for (int j = 0; j < kSegDims; ++j) { K.st[j] = 0; K.ex[j] = 1; }
+#pragma unroll
+  for (int d = 0; d < kSegDims; ++d) {
+    if (d >= L.nd || ((smask >> d) & 1u)) continue;
+#pragma unroll
+    for (int j = 0; j < kSegDims; ++j)
+      if (j == K.nd) { K.st[j] = L.st[d]; K.ex[j] = L.ex[d]; }
+    ++K.nd;
+  }
+  for (int64_t m = 0; m < combos; ++m) {
+    int64_t r = m;
+    uint64_t b = (uint64_t)L.base;
+#pragma unroll
+    for (int d = 0; d < kSegDims; ++d) {
+      if (!((smask >> d) & 1u)) continue;
+      b += L.st[d] * (uint64_t)(r % L.ex[d]);
+      r /= L.ex[d];
+    }
+    K.base = (int64_t)b;
+    l4_emit_normalized(S, K, tag, G);
+  }
 }
 
 // Pattern run (Run::kind 2): rows of cells along a stride s0 in which every
@@ -274,36 +526,59 @@ __device__ inline void emit_normalized(const RunSink& S, const Lat& L, int tag, 
 // per row, its interval spans the row, and the bitmap tier sets the row's
 // sectors from the periodic per-period pattern (lcm(s0, g) / g sectors) word
 // by word instead of one interval per cell and residue cluster.  Returns
-// false (nothing emitted) when the rows would not be monotone.
+// false (nothing emitted) when the rows would not be monotone.  Per lane.
 constexpr int64_t kPatMinCells = 32;
 __device__ inline int64_t gcd64(int64_t a, int64_t b);
 __device__ __forceinline__ uint32_t pattern_bits(int64_t cell0, uint64_t pm, int64_t dg, int64_t s0, int64_t P,
                                                  int64_t nph, int64_t g, int shift, int part, int nparts);
-__device__ inline bool emit_pattern(const RunSink& S, const Lat& Lbox, uint64_t cell0, int tag, const Granule& G,
+__device__ inline bool emit_pattern(const RunSink& S, const Lat4& Lbox, uint64_t cell0, int tag, const Granule& G,
                                     uint64_t pm, int64_t dg, int64_t s0) {
   int64_t n0 = Lbox.ex[0];
-  Lat L;  // outer dims (rows), sorted, rows that continue the cell sequence merged into n0
-  L.nd = 0;
-  for (int d = 1; d < Lbox.nd; ++d)
-    if (Lbox.ex[d] > 1) { L.st[L.nd] = Lbox.st[d]; L.ex[L.nd] = Lbox.ex[d]; ++L.nd; }
-  sort_dims(L);
-  while (L.nd > 0 && L.st[0] == (uint64_t)(n0 * s0)) {
-    n0 *= L.ex[0];
-    for (int i = 1; i < L.nd; ++i) { L.st[i - 1] = L.st[i]; L.ex[i - 1] = L.ex[i]; }
-    --L.nd;
+  // outer dims (rows) with ex > 1, sorted by stride (rank sort, static indices)
+  uint64_t s[kSegDims - 1];
+  int64_t e[kSegDims - 1];
+#pragma unroll
+  for (int d = 1; d < kSegDims; ++d) {
+    const bool ok = d < Lbox.nd && Lbox.ex[d] > 1;
+    s[d - 1] = ok ? Lbox.st[d] : ~0ull;
+    e[d - 1] = ok ? Lbox.ex[d] : 1;
   }
+  l4_cswap(s[0], e[0], s[1], e[1]);
+  l4_cswap(s[1], e[1], s[2], e[2]);
+  l4_cswap(s[0], e[0], s[1], e[1]);
+  int nd = 0;
+#pragma unroll
+  for (int d = 0; d < kSegDims - 1; ++d) nd += s[d] != ~0ull;
+  // rows that continue the cell sequence merge into n0
+  int k = 0;
+#pragma unroll
+  for (int d = 0; d < kSegDims - 1; ++d) {
+    if (k == d && d < nd && s[d] == (uint64_t)(n0 * s0)) { n0 *= e[d]; ++k; }
+  }
+  uint64_t rs[kSegDims - 1];
+  int64_t re[kSegDims - 1];
+#pragma unroll
+  for (int j = 0; j < kSegDims - 1; ++j) {
+    rs[j] = 0; re[j] = 1;
+#pragma unroll
+    for (int q = 0; q < kSegDims - 1; ++q)
+      if (q == j + k) { rs[j] = s[q]; re[j] = e[q]; }
+  }
+  nd -= k;
   if (n0 >= (int64_t(1) << 31)) return false;
   const int64_t rmin = (int64_t)__ffsll((long long)pm) - 1, rmax = 63 - __clzll((long long)pm);
   const uint64_t span = (uint64_t)((n0 - 1) * s0 + (rmax - rmin) * dg);
   unsigned __int128 reach = span;
   int64_t count = 1;
   uint64_t ext_span = span;
-  for (int d = 0; d < L.nd; ++d) {
-    if ((unsigned __int128)L.st[d] <= reach) return false;  // rows must be monotone
-    reach += (unsigned __int128)L.st[d] * (uint64_t)(L.ex[d] - 1);
-    if (count > (int64_t(1) << 40) / L.ex[d]) return false;
-    count *= L.ex[d];
-    ext_span += L.st[d] * (uint64_t)(L.ex[d] - 1);
+#pragma unroll
+  for (int d = 0; d < kSegDims - 1; ++d) {
+    if (d >= nd) continue;
+    if ((unsigned __int128)rs[d] <= reach) return false;  // rows must be monotone
+    reach += (unsigned __int128)rs[d] * (uint64_t)(re[d] - 1);
+    if (count > (int64_t(1) << 40) / re[d]) return false;
+    count *= re[d];
+    ext_span += rs[d] * (uint64_t)(re[d] - 1);
   }
   const int slot = atomicAdd(S.n_runs, 1);
   if (slot >= S.cap) { atomicExch(S.status, GVO_ERR_CAPACITY); return true; }
@@ -311,10 +586,11 @@ __device__ inline bool emit_pattern(const RunSink& S, const Lat& Lbox, uint64_t 
   Run* r = S.runs + slot;
   r->base = (int64_t)base;
   r->span = span;
-  r->nd = L.nd;
+  r->nd = nd;
+#pragma unroll
   for (int d = 0; d < kMaxDims; ++d) {
-    r->stride[d] = d < L.nd ? (int64_t)L.st[d] : 0;
-    r->ext[d] = d < L.nd ? L.ex[d] : 1;
+    r->stride[d] = d < kSegDims - 1 && d < nd ? (int64_t)rs[d < kSegDims - 1 ? d : 0] : 0;
+    r->ext[d] = d < kSegDims - 1 && d < nd ? re[d < kSegDims - 1 ? d : 0] : 1;
   }
   r->tag = tag;
   r->kind = 2;
@@ -341,46 +617,63 @@ __device__ inline int64_t gcd64(int64_t a, int64_t b) {  // a, b >= 0
   return a;
 }
 
-// Warp-cooperative version: the class's translates P[0..n) (n <= 64, sorted,
-// unique) live in shared memory.  Rays of one dimension are disjoint (every
-// point starts or continues exactly one maximal ray along that stride), so
-// all rays of a dimension are judged in parallel against the points not yet
-// covered by larger-stride rays; the same greedy as cover_and_emit.
-__device__ GVO_NOINL void cover_warp(const RunSink& S, const Lat& L0, const int64_t* P, int n, int tag,
-                           const Granule& G) {
+// Maximal ray from translate i along stride s: members (bitmask over P) and
+// length.  P sorted and unique.
+__device__ __forceinline__ int ray_from(const int64_t* P, int n, int i, int64_t s, uint64_t* mem_out) {
+  uint64_t mem = 1ull << i;
+  int len = 1, pos = i;
+  while (pos + 1 < n) {
+    // the successor v + s, if present, is after pos
+    const int64_t t = P[pos] + s;
+    int lo = pos + 1, hi = n - 1, f = -1;
+    while (lo <= hi) {
+      const int mid = (lo + hi) >> 1;
+      if (P[mid] == t) { f = mid; break; }
+      if (P[mid] < t) lo = mid + 1; else hi = mid - 1;
+    }
+    if (f < 0) break;
+    mem |= 1ull << f;
+    ++len;
+    pos = f;
+  }
+  *mem_out = mem;
+  return len;
+}
+
+// Translate cover of one coefficient class: the class's translates P[0..n)
+// (n <= 64, sorted, unique) live in shared memory.  Rays of one dimension
+// are disjoint (every point starts or continues exactly one maximal ray
+// along that stride), so all rays of a dimension are judged in parallel
+// (lane per translate) against the points not yet covered by larger-stride
+// rays; the warp then emits them one after another.
+__device__ GVO_NOINL void cover_warp(const RunSink& S, const WLat& L0, const int64_t* P, int n, int tag,
+                                     const Granule& G) {
   const int lane = threadIdx.x & 31;
   uint64_t req = n >= 64 ? ~0ull : ((1ull << n) - 1);
   for (int d = L0.nd - 1; d >= 0 && req; --d) {
-    const int64_t s = (int64_t)L0.st[d];
+    const int64_t s = (int64_t)__shfl_sync(kFull, L0.st, d);
     uint64_t clear = 0;
-    for (int i = lane; i < n; i += 32) {
-      if (contains(P, n, P[i] - s)) continue;  // not a ray start
-      uint64_t mem = 1ull << i;
-      int len = 1, pos = i;
-      while (pos + 1 < n) {
-        // the successor v + s, if present, is after pos
-        const int64_t t = P[pos] + s;
-        int lo = pos + 1, hi = n - 1, f = -1;
-        while (lo <= hi) {
-          const int mid = (lo + hi) >> 1;
-          if (P[mid] == t) { f = mid; break; }
-          if (P[mid] < t) lo = mid + 1; else hi = mid - 1;
-        }
-        if (f < 0) break;
-        mem |= 1ull << f;
-        ++len;
-        pos = f;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      bool ray = false;
+      int len = 0;
+      uint64_t mem = 0;
+      if (i < n && !contains(P, n, P[i] - s)) {  // a ray start
+        len = ray_from(P, n, i, s, &mem);
+        ray = len >= 2 && __popcll(mem & req) >= 2;
       }
-      if (len >= 2 && __popcll(mem & req) >= 2) {
-        Lat L = L0;
-        L.base = P[i];
-        L.ex[d] += len - 1;
-        emit_lattice(S, L, tag, G);
-        clear |= mem;
+      if (ray) clear |= mem;
+      for (unsigned rm = __ballot_sync(kFull, ray); rm; rm &= rm - 1) {
+        const int src = __ffs(rm) - 1;
+        WLat L = L0;
+        L.base = __shfl_sync(kFull, i < n ? P[i < n ? i : 0] : 0, src);
+        const int ln = __shfl_sync(kFull, len, src);
+        if (lane == d) L.ex += ln - 1;
+        wl_emit_lattice(S, L, tag, G);
       }
     }
-    const unsigned lo32 = __reduce_or_sync(0xffffffffu, (unsigned)clear);
-    const unsigned hi32 = __reduce_or_sync(0xffffffffu, (unsigned)(clear >> 32));
+    const unsigned lo32 = __reduce_or_sync(kFull, (unsigned)clear);
+    const unsigned hi32 = __reduce_or_sync(kFull, (unsigned)(clear >> 32));
     req &= ~(((uint64_t)hi32 << 32) | lo32);
   }
   // rays along a stride that is not a lattice dimension (e.g. +-z offsets of
@@ -395,54 +688,55 @@ __device__ GVO_NOINL void cover_warp(const RunSink& S, const Lat& L0, const int6
       while (k < n && !((req >> k) & 1ull)) ++k;
       if (k < n) gap = min(gap, P[k] - P[i]);
     }
-    for (int o = 16; o; o >>= 1) gap = min(gap, __shfl_xor_sync(0xffffffffu, gap, o));
+    for (int o = 16; o; o >>= 1) gap = min(gap, __shfl_xor_sync(kFull, gap, o));
     if (gap == INT64_MAX || (unsigned __int128)(uint64_t)gap <= tol0) break;
     uint64_t clear = 0;
-    for (int i = lane; i < n; i += 32) {
-      if (contains(P, n, P[i] - gap)) continue;
-      uint64_t mem = 1ull << i;
-      int len = 1, pos = i;
-      while (pos + 1 < n) {
-        const int64_t t = P[pos] + gap;
-        int lo = pos + 1, hi = n - 1, f = -1;
-        while (lo <= hi) {
-          const int mid = (lo + hi) >> 1;
-          if (P[mid] == t) { f = mid; break; }
-          if (P[mid] < t) lo = mid + 1; else hi = mid - 1;
-        }
-        if (f < 0) break;
-        mem |= 1ull << f;
-        ++len;
-        pos = f;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      bool ray = false;
+      int len = 0;
+      uint64_t mem = 0;
+      if (i < n && !contains(P, n, P[i] - gap)) {
+        len = ray_from(P, n, i, gap, &mem);
+        ray = len >= 2 && __popcll(mem & req) >= 2;
       }
-      if (len >= 2 && __popcll(mem & req) >= 2) {
-        Lat L = L0;
-        L.base = P[i];
-        L.st[L.nd] = (uint64_t)gap;
-        L.ex[L.nd] = len;
-        ++L.nd;
-        emit_lattice(S, L, tag, G);
-        clear |= mem;
+      if (ray) clear |= mem;
+      for (unsigned rm = __ballot_sync(kFull, ray); rm; rm &= rm - 1) {
+        const int src = __ffs(rm) - 1;
+        WLat L = L0;
+        L.base = __shfl_sync(kFull, i < n ? P[i < n ? i : 0] : 0, src);
+        const int ln = __shfl_sync(kFull, len, src);
+        if (lane == L0.nd) { L.st = (uint64_t)gap; L.ex = ln; }
+        L.nd = L0.nd + 1;
+        wl_emit_lattice(S, L, tag, G);
       }
     }
-    const unsigned lo32 = __reduce_or_sync(0xffffffffu, (unsigned)clear);
-    const unsigned hi32 = __reduce_or_sync(0xffffffffu, (unsigned)(clear >> 32));
+    const unsigned lo32 = __reduce_or_sync(kFull, (unsigned)clear);
+    const unsigned hi32 = __reduce_or_sync(kFull, (unsigned)(clear >> 32));
     const uint64_t cl = ((uint64_t)hi32 << 32) | lo32;
     if (!cl) break;
     req &= ~cl;
   }
   if (!req) return;
+  // clusters: consecutive translates closer than span + g widen the span
   const unsigned __int128 tol = (unsigned __int128)L0.span + (uint64_t)G.g;
-  for (int i = lane; i < n; i += 32) {
-    if (i > 0 && (unsigned __int128)(uint64_t)(P[i] - P[i - 1]) <= tol) continue;  // not a cluster start
-    int j = i;
-    uint64_t mem = 1ull << i;
-    while (j + 1 < n && (unsigned __int128)(uint64_t)(P[j + 1] - P[j]) <= tol) { ++j; mem |= 1ull << j; }
-    if (mem & req) {
-      Lat L = L0;
-      L.base = P[i];
-      L.span = L0.span + (uint64_t)(P[j] - P[i]);
-      emit_lattice(S, L, tag, G);
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    bool start = false;
+    int64_t width = 0;
+    if (i < n && !(i > 0 && (unsigned __int128)(uint64_t)(P[i] - P[i - 1]) <= tol)) {
+      int j = i;
+      uint64_t mem = 1ull << i;
+      while (j + 1 < n && (unsigned __int128)(uint64_t)(P[j + 1] - P[j]) <= tol) { ++j; mem |= 1ull << j; }
+      start = (mem & req) != 0;
+      width = P[j] - P[i];
+    }
+    for (unsigned rm = __ballot_sync(kFull, start); rm; rm &= rm - 1) {
+      const int src = __ffs(rm) - 1;
+      WLat L = L0;
+      L.base = __shfl_sync(kFull, i < n ? P[i < n ? i : 0] : 0, src);
+      L.span = L0.span + (uint64_t)__shfl_sync(kFull, width, src);
+      wl_emit_lattice(S, L, tag, G);
     }
   }
 }
@@ -460,8 +754,7 @@ __device__ GVO_NOINL void cover_warp(const RunSink& S, const Lat& L0, const int6
 // translate is present the cluster covers a whole cell, folds into the span
 // and rows collapse into intervals.  Exact: the segment boxes partition the
 // union of the B_p (any decomposition of the offsets is valid).
-constexpr int kSegDims = 4;
-constexpr int kSegBpAll = 264;      // breakpoints over all dimensions (flat)
+constexpr int kSegBpAll = 248;      // breakpoints over all dimensions (flat)
 constexpr int kSegMaxBoxes = 4096;
 constexpr int kSegScratch = 2688;   // bytes of per-warp scratch
 #ifndef GVO_SEG_RUN_WEIGHT
@@ -469,6 +762,8 @@ constexpr int kSegScratch = 2688;   // bytes of per-warp scratch
 #endif
 constexpr int64_t kSegRunWeight = GVO_SEG_RUN_WEIGHT;  // element-equivalents of one extra run (A/B on C3: 16 > 32 > 48 > 100)
 struct SegScratch {
+  uint64_t l0st[kSegDims];   // the class lattice's dims (read by any lane)
+  int64_t l0ex[kSegDims];
   int32_t kv[kSegDims][64];  // offsets per dimension, by translate
   int32_t bpf[kSegBpAll];    // breakpoints, dimension d at boff[d]
   int32_t boff[kSegDims];
@@ -489,15 +784,20 @@ __device__ __forceinline__ int64_t floordiv128(__int128 a, __int128 b, __int128*
 
 // Returns false (nothing emitted) when the class is not of that shape or
 // the segment plan is not cheaper than cover_warp's.
-__device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, const int64_t* P, int n, int tag,
+__device__ __noinline__ bool cover_segments(const RunSink& S, const WLat& L0, const int64_t* P, int n, int tag,
                                const Granule& G, SegScratch* sc, bool allow_pattern) {
   const int lane = threadIdx.x & 31;
   const int nd = L0.nd;
   if (nd < 1 || nd > kSegDims || n < 2 || n > 64) return false;
-  const uint64_t s0 = L0.st[0];
+  const uint64_t s0 = __shfl_sync(kFull, L0.st, 0);
   if (s0 >= (uint64_t(1) << 30) || L0.span >= s0) return false;
-  for (int d = 0; d < nd; ++d)
-    if (L0.ex[d] >= (int64_t(1) << 29) || L0.st[d] >= (uint64_t(1) << 62)) return false;
+  if (__any_sync(kFull, lane < nd && (L0.ex >= (int64_t(1) << 29) || L0.st >= (uint64_t(1) << 62)))) return false;
+  __syncwarp();
+  if (lane < kSegDims) {
+    sc->l0st[lane] = lane < nd ? L0.st : 0;
+    sc->l0ex[lane] = lane < nd ? L0.ex : 1;
+  }
+  __syncwarp();
   const int64_t tol = (int64_t)L0.span + G.g;
   if ((int64_t)n * tol < (int64_t)s0) return false;  // n residues cannot tile a cell
   {  // cheap screen: distinct residues mod s0 (one match per lane) must be able to tile it
@@ -520,7 +820,7 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
     if (off0 > -(__int128(1) << 60) && off0 < (__int128(1) << 60)) {
       int64_t off = (int64_t)off0;  // strides < 2^62: no overflow below
       for (int d = nd - 1; d >= 1; --d) {
-        const int64_t s = (int64_t)L0.st[d];
+        const int64_t s = (int64_t)sc->l0st[d];
         const int64_t k = floordiv(off + s / 2, s);
         off -= k * s;
         if (k < -(int64_t(1) << 28) || k > (int64_t(1) << 28)) ok = false;
@@ -533,7 +833,7 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
     } else {
       __int128 off = off0, rem;
       for (int d = nd - 1; d >= 1; --d) {
-        const __int128 s = (__int128)L0.st[d];
+        const __int128 s = (__int128)sc->l0st[d];
         const int64_t k = floordiv128(off + s / 2, s, &rem);
         off -= (__int128)k * s;
         if (k < -(int64_t(1) << 28) || k > (int64_t(1) << 28)) ok = false;
@@ -579,7 +879,7 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
   // 3. breakpoints per dimension: distinct offsets D, merged with D + ex
   int64_t nbox = 1;
   for (int d = 0; d < nd; ++d) {
-    const int32_t ex = (int32_t)L0.ex[d];
+    const int32_t ex = (int32_t)sc->l0ex[d];
     int32_t v[2];
     int rk[2];
     for (int t = 0; t < 2; ++t) {
@@ -672,7 +972,7 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
       const int sg = lane + 32 * h;
       if (!fly && d < nd && sg < sc->nb[d] - 1) {
         const int32_t lo = sc->bpf[sc->boff[d] + (sg)], hi = sc->bpf[sc->boff[d] + (sg + 1)];
-        const int32_t ex = (int32_t)L0.ex[d];
+        const int32_t ex = (int32_t)sc->l0ex[d];
         for (int r = 0; r < n; ++r) {
           const int32_t k = sc->kv[d][sc->ord[r]];
           if (k <= lo && hi <= k + ex) segm[d][h] |= 1ull << r;
@@ -682,7 +982,7 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
   }
   // 5. plan: elements and runs of the segment cover vs. cover_warp's clusters
   double vol0 = 1.0;
-  for (int d = 0; d < nd; ++d) vol0 *= (double)L0.ex[d];
+  for (int d = 0; d < nd; ++d) vol0 *= (double)sc->l0ex[d];
   double seg_el = 0.0;
   int64_t seg_runs = 0;
   for (int64_t b0 = 0; b0 < nbox; b0 += 32) {
@@ -709,7 +1009,7 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
         bool in = true;
         for (int d = 0; d < nd && in; ++d) {
           const int32_t k = sc->kv[d][sc->ord[r2]];
-          in = k <= sc->bpf[sc->boff[d] + sd[d]] && sc->bpf[sc->boff[d] + sd[d] + 1] <= k + (int32_t)L0.ex[d];
+          in = k <= sc->bpf[sc->boff[d] + sd[d]] && sc->bpf[sc->boff[d] + sd[d] + 1] <= k + (int32_t)sc->l0ex[d];
         }
         if (in) M |= 1ull << r2;
       }
@@ -768,20 +1068,28 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
         bool in = true;
         for (int d = 0; d < nd && in; ++d) {
           const int32_t k = sc->kv[d][sc->ord[r2]];
-          in = k <= sc->bpf[sc->boff[d] + sd[d]] && sc->bpf[sc->boff[d] + sd[d] + 1] <= k + (int32_t)L0.ex[d];
+          in = k <= sc->bpf[sc->boff[d] + sd[d]] && sc->bpf[sc->boff[d] + sd[d] + 1] <= k + (int32_t)sc->l0ex[d];
         }
         if (in) M |= 1ull << r2;
       }
     }
     if (b >= nbox || !M) continue;
-    Lat L;
+    Lat4 L;
     L.nd = nd;
+    L.span = L0.span;
     uint64_t base = (uint64_t)L0.base;
-    for (int d = 0; d < nd; ++d) {
-      L.st[d] = L0.st[d];
-      L.ex[d] = (int64_t)(sc->bpf[sc->boff[d] + sd[d] + 1] - sc->bpf[sc->boff[d] + sd[d]]);
-      base += L0.st[d] * (uint64_t)(int64_t)sc->bpf[sc->boff[d] + sd[d]];
+#pragma unroll
+    for (int d = 0; d < kSegDims; ++d) {
+      if (d < nd) {
+        L.st[d] = sc->l0st[d];
+        L.ex[d] = (int64_t)(sc->bpf[sc->boff[d] + sd[d] + 1] - sc->bpf[sc->boff[d] + sd[d]]);
+        base += sc->l0st[d] * (uint64_t)(int64_t)sc->bpf[sc->boff[d] + sd[d]];
+      } else {
+        L.st[d] = 0;
+        L.ex[d] = 1;
+      }
     }
+    L.base = (int64_t)base;
     // partial cells along a long row: one pattern run instead of one
     // lattice per residue cluster (unless the clusters fold into the span)
     if (allow_pattern && L0.span == 0 && L.ex[0] >= kPatMinCells) {
@@ -814,37 +1122,35 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const Lat& L0, con
         r1 = q;
         mm &= mm - 1;
       }
-      Lat C = L;
+      Lat4 C = L;
       C.base = (int64_t)(base + (uint64_t)(int64_t)sc->rs[r0]);
       C.span = L0.span + (uint64_t)(sc->rs[r1] - sc->rs[r0]);
-      emit_lattice(S, C, tag, G);
+      l4_emit_lattice(S, C, tag, G);
     }
   }
   return true;
 }
 
 // lattice of one coefficient vector over one block box, translation 0
-__device__ inline Lat box_lattice(const int64_t* c, const int32_t bd[3], const Box& b, const Granule& G) {
-  Lat L;
-  const int64_t ext[6] = {bd[0], bd[1], bd[2], b.n[0], b.n[1], b.n[2]};
-  uint64_t base = (uint64_t)c[4] * (uint64_t)b.lo[0] + (uint64_t)c[5] * (uint64_t)b.lo[1] +
-                  (uint64_t)c[6] * (uint64_t)b.lo[2];
-  L.nd = 0;
-  L.span = 0;
-  for (int k = 0; k < 6; ++k) {
-    int64_t co = c[1 + k];
-    if (ext[k] <= 1 || co == 0) continue;
-    if (co < 0) {
-      base += (uint64_t)co * (uint64_t)(ext[k] - 1);
-      L.st[L.nd] = (uint64_t)0 - (uint64_t)co;
-    } else {
-      L.st[L.nd] = (uint64_t)co;
-    }
-    L.ex[L.nd] = ext[k];
-    ++L.nd;
+// (warp-cooperative: lane k < 6 holds coordinate k = tid x/y/z, bid x/y/z)
+__device__ inline WLat box_lattice(const int64_t* c, const int32_t bd[3], const Box& b, const Granule& G) {
+  const int lane = threadIdx.x & 31;
+  int64_t ext = 1, co = 0;
+  uint64_t contrib = 0;
+  if (lane < 6) {
+    ext = lane == 0 ? bd[0] : lane == 1 ? bd[1] : lane == 2 ? bd[2] : lane == 3 ? b.n[0] : lane == 4 ? b.n[1] : b.n[2];
+    co = c[1 + lane];
+    if (lane >= 3) contrib = (uint64_t)co * (uint64_t)(lane == 3 ? b.lo[0] : lane == 4 ? b.lo[1] : b.lo[2]);
+    if (ext > 1 && co < 0) contrib += (uint64_t)co * (uint64_t)(ext - 1);
   }
-  L.base = (int64_t)base;
-  normalize(L, G.g);
+  for (int o = 4; o; o >>= 1) contrib += __shfl_xor_sync(kFull, contrib, o);
+  WLat L;
+  L.base = (int64_t)__shfl_sync(kFull, contrib, 0);
+  L.span = 0;
+  L.nd = 6;
+  L.st = lane < 6 && ext > 1 && co != 0 ? (co < 0 ? (uint64_t)0 - (uint64_t)co : (uint64_t)co) : 0;
+  L.ex = lane < 6 ? ext : 1;
+  wl_normalize(L, G.g);
   return L;
 }
 
@@ -908,25 +1214,35 @@ __device__ inline int64_t mono_first(const Run& r, const Granule& Gr, int64_t kb
   // f(k) = base + sum_d stride_d k_d increases with the tuple index (the
   // monotone condition), so floor((f + span?)/g) - kbase >= v <=> f >= T:
   // the digits of the first such tuple follow greedily from the slowest dim.
+  // Loops over dims are unrolled with constant indices (registers only).
   const __int128 T = ((__int128)v + (__int128)kbase) * (__int128)Gr.g - (hi ? (__int128)r.span : (__int128)0);
   const __int128 R0 = T - (__int128)r.base;
   if (R0 <= 0) return 0;
-  int64_t M[kMaxDims];  // reach of the dims faster than d
+  const int nd = r.nd;
+  int64_t st[kMaxDims], ex[kMaxDims], M[kMaxDims];  // M[d]: reach of the dims faster than d
   uint64_t acc = 0;
-  for (int d = 0; d < r.nd; ++d) { M[d] = (int64_t)acc; acc += (uint64_t)r.stride[d] * (uint64_t)(r.ext[d] - 1); }
+#pragma unroll
+  for (int d = 0; d < kMaxDims; ++d) {
+    st[d] = d < nd ? r.stride[d] : 0;
+    ex[d] = d < nd ? r.ext[d] : 1;
+    M[d] = (int64_t)acc;
+    acc += (uint64_t)st[d] * (uint64_t)(ex[d] - 1);
+  }
   if (R0 > (__int128)acc) return r.count;
   int64_t R = (int64_t)R0;
   int64_t mul = 1;
-  for (int d = 0; d < r.nd; ++d) mul *= r.ext[d];
+#pragma unroll
+  for (int d = 0; d < kMaxDims; ++d) mul *= ex[d];
   int64_t idx = 0;
-  for (int d = r.nd - 1; d >= 0; --d) {
-    mul /= r.ext[d];
+#pragma unroll
+  for (int d = kMaxDims - 1; d >= 0; --d) {
+    mul /= ex[d];
     int64_t k = 0;
-    if (R > M[d]) {
-      const uint64_t st = (uint64_t)r.stride[d];
-      k = (int64_t)(((uint64_t)(R - M[d]) + st - 1) / st);
-      if (k > r.ext[d] - 1) k = r.ext[d] - 1;
-      R -= (int64_t)((uint64_t)k * st);
+    if (d < nd && R > M[d]) {
+      const uint64_t s1 = (uint64_t)st[d];
+      k = (int64_t)(((uint64_t)(R - M[d]) + s1 - 1) / s1);
+      if (k > ex[d] - 1) k = ex[d] - 1;
+      R -= (int64_t)((uint64_t)k * s1);
     }
     idx += k * mul;
   }
@@ -1671,7 +1987,7 @@ __device__ bool micro_unit(const SetsArgs& P, int64_t bidx, uint8_t* reg, int64_
     const int64_t cl0 = ct.slot_first()[slot], cl1 = ct.slot_first()[slot + 1];
     for (int64_t cls = cl0; cls < cl1; ++cls) {
       const int64_t* ca = crow + ct.rep()[cls] * 8;
-      const Lat L0 = box_lattice(ca, bd, box, Gr);
+      const WLat L0 = box_lattice(ca, bd, box, Gr);
       const int64_t* cp = ct.pts() + ct.start()[cls];
       const int64_t np = ct.cnt()[cls];
       for (int64_t p0 = 0; p0 < np; p0 += kClassPts) {
@@ -2178,8 +2494,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
             const int slot = slot0 + U.src_kind[s2];
             const int nc = (int)(ct.slot_first()[slot + 1] - ct.slot_first()[slot]);
             if (nc <= 0) continue;
-            Box bx[5];
-            const int nb = run_boxes(U.src_start[s2], U.src_count[s2], gd, bx);
+            const int nb = run_box_count(U.src_start[s2], U.src_count[s2], gd);
             for (int bi = 0; bi < nb && nt >= 0; ++bi)
               for (int ci = 0; ci < nc; ++ci) {
                 if (nt >= tcap) { nt = -1; break; }
@@ -2203,12 +2518,11 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           const int slot = slot0 + U.src_kind[s];
           const int64_t cl0 = ct.slot_first()[slot];
           if (ci >= ct.slot_first()[slot + 1] - cl0) continue;
-          Box boxes[5];
-          const int nb = run_boxes(U.src_start[s], U.src_count[s], gd, boxes);
-          if (bi >= nb) continue;
+          Box box;
+          if (!run_box_at(U.src_start[s], U.src_count[s], gd, bi, &box)) continue;
           const int64_t cls = cl0 + ci;
           const int64_t* ca = crow + ct.rep()[cls] * 8;
-          const Lat L0 = box_lattice(ca, bd, boxes[bi], Gr);
+          const WLat L0 = box_lattice(ca, bd, box, Gr);
           const int64_t* cp = ct.pts() + ct.start()[cls];
           const int64_t np = ct.cnt()[cls];
           for (int64_t p0 = 0; p0 < np; p0 += kClassPts) {

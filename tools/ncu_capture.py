@@ -105,8 +105,12 @@ def main():
     full = out_dir / f"ncu_full_k_sets_{wl.lower()}.csv"
     skip = max(0, sets["launches"] // 2)
     r = subprocess.run([NCU, "--set", "full", "--clock-control", "none", "-k", "regex:k_sets", "--launch-skip",
-                        str(skip), "--launch-count", "1", "--import-source", "on", "--csv", "--page", "raw",
-                        "--log-file", str(full), *bench], cwd=ROOT)
+                        str(skip), "--launch-count", "1", "--import-source", "on",
+                        "--export", str(out_dir / f"ncu_k_sets_{wl.lower()}"), "--force-overwrite", *bench], cwd=ROOT)
+    if r.returncode == 0:
+        raw_txt = subprocess.run([NCU, "-i", str(out_dir / f"ncu_k_sets_{wl.lower()}.ncu-rep"), "--page", "raw",
+                                  "--csv"], capture_output=True, text=True).stdout
+        full.write_text(raw_txt)
     if r.returncode == 0 and full.exists():
         raw = list(csv.reader(io.StringIO("\n".join(ln for ln in full.read_text().splitlines()
                                                      if ln.startswith('"')))))
