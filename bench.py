@@ -294,6 +294,7 @@ def run_device(args, rank, world):
     kcnt = (C.c_int64 * 8)()
     L.gvo_kernel_times(ctx.h, kms, kcnt, 1)
     L.gvo_set_timing(ctx.h, 0)
+    sharing = sharing_leg(ctx, step, stream, flush, n) if not args.no_e2e else None
     per_rank = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         allr = _gather_np(np.array([ms]), world)
@@ -377,6 +378,7 @@ def run_device(args, rank, world):
         "launches_per_step": {k: v / max(1, args.steps) for k, v in launches.items()},
         "kernel_ms_per_step": kernel_ms,
         "e2e_api": api,
+        "sharing": sharing,
         "rank_ms": ms_all if world > 1 else None,
         "roofline": roof,
         "cpu_baseline": cpu,
@@ -385,6 +387,44 @@ def run_device(args, rank, world):
         "build_id": bid,
     }
     print(json.dumps(line), flush=True)
+
+
+def sharing_leg(ctx, step, stream, flush, n):
+    """Cross-configuration sharing of identical set problems (k_dedup.cu)
+    is part of every timed step above.  Here: how much of the step it
+    shared (one counted step), and the same step with sharing switched off
+    (one step, CUDA events, same L2 flush) -- the rate of an engine that
+    evaluates every configuration from scratch."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2107_01143_b200 import _native
+
+    L = _native.lib()
+    L.gvo_dedup_stats(ctx.h, 1, None, None)
+    step()
+    torch.cuda.synchronize()
+    units, follow = C.c_int64(), C.c_int64()
+    L.gvo_dedup_stats(ctx.h, 0, C.byref(units), C.byref(follow))
+    ctx.check(L.gvo_set_dedup(ctx.h, 0))
+    try:
+        step()  # warm the unshared path
+        flush.fill_(7)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms_off = a.elapsed_time(b)
+    finally:
+        ctx.check(L.gvo_set_dedup(ctx.h, 1))
+    return {"shareable_units": units.value, "units_copied": follow.value,
+            "copied_fraction": follow.value / units.value if units.value else 0.0,
+            "no_sharing": {"value": n / (ms_off * 1e-3), "unit": "configs/s", "ms_per_step": ms_off, "steps": 1},
+            "note": "units = (config, field) wave sets, (config, field, sample) block sets, (config, sample) "
+                    "warp/L1 items; a copied unit is an exact translate of one computed in the same call "
+                    "(same accesses up to the field base, base residue, launch and machine integer parameters)"}
 
 
 def api_leg(ctx, smp, reps: int = 5):

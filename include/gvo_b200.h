@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define GVO_ABI_VERSION 2
+#define GVO_ABI_VERSION 3
 
 /* ---- status codes: map 1:1 onto the reference's exception classes ---- */
 enum gvo_status {
@@ -349,6 +349,16 @@ int gvo_kernel_times(gvo_ctx* ctx, double* ms_out, int64_t* count_out, int reset
  * fetch those of the last batch: [item][runs, intervals, in-smem, cycles,
  * key bits, SM id]; items ordered (config, field, unit). */
 int gvo_debug_units(gvo_ctx* ctx, int enable, int64_t* h_out, int64_t cap, int64_t* n_items);
+/* Cross-configuration sharing of identical set problems (every
+ * gvo_eval_configs* call; GVO_DEDUP=0 in the environment of gvo_open turns it
+ * off).  enable_counting != 0 makes later calls count, and this returns the
+ * last call's figures: units eligible for sharing and units that copied an
+ * identical unit's counts instead of computing them.  Returns 1 when sharing
+ * is on, 0 when off.  (No reference counterpart: the reference evaluates every
+ * configuration from scratch, perf.py:115-130; results are identical.) */
+int gvo_dedup_stats(gvo_ctx* ctx, int enable_counting, int64_t* shareable_units, int64_t* followers);
+/* Turn the sharing on (1) or off (0) for later calls on this context. */
+int gvo_set_dedup(gvo_ctx* ctx, int enable);
 /* Measured INT32 issue rate of the device (ops/s), the integer roofline. */
 int gvo_int_peak(gvo_ctx* ctx, double* ops_per_s);
 

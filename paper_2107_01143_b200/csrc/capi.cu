@@ -3,6 +3,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 #include <nvtx3/nvToolsExt.h>
 #include "gvo_kernels.h"
@@ -77,11 +78,21 @@ struct gvo_ctx {
   std::vector<int32_t> h_nacc, h_nfields;
   DBuf<int32_t> t_nf, t_na, t_ab, t_fbo, t_af, t_ak, t_co, t_cl, t_fko, t_fkl;
   DBuf<int64_t> t_fb, t_am;
+  DBuf<int32_t> t_fcls, t_tcls;  // translation classes (k_dedup.cu)
   DBuf<gvo_insn> t_code;
   TplView view{};
   // machines
   std::vector<gvo_machine> h_machines;
   DBuf<gvo_machine> d_machines;
+  DBuf<int32_t> d_mclass;  // machines with equal integer parameters share a class
+  // cross-configuration sharing of identical set problems (k_dedup.cu):
+  // GVO_DEDUP=0 evaluates every unit of every configuration
+  bool dedup = true;
+  DBuf<DedupEntry> dd_table;
+  int64_t dd_mask = 0;
+  DBuf<int64_t> dd_lead;
+  int64_t dd_units = 0, dd_follow = 0;  // last call: units, followers (gvo_dedup_stats)
+  bool dd_count = false;
   // work
   DBuf<int64_t> coefs;
   DBuf<int64_t> ctabs;
@@ -167,6 +178,91 @@ static int set_err(gvo_ctx* ctx, int code, const char* fmt, const char* detail =
 
 static cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// ---- translation classes (k_dedup.cu)
+// Access `a` of field f is translation-safe when its value is exactly
+// base_f + E(coordinates, block dims) with E free of every field base: the
+// base enters through additions/subtractions only, with coefficient 1, never
+// through *, // or % and no other field's base appears.  Moving base_f by Δ
+// then moves every address of the field by Δ.
+static bool base_additive(const gvo_insn* code, int len, int f) {
+  int64_t st[64];
+  int sp = 0;
+  for (int i = 0; i < len; ++i) {
+    const gvo_insn& in = code[i];
+    if (in.op <= GVO_OP_BASE) {
+      if (sp >= 64) return false;
+      if (in.op == GVO_OP_BASE && in.arg != f) return false;
+      st[sp++] = in.op == GVO_OP_BASE ? 1 : 0;
+      continue;
+    }
+    if (sp < 2) return false;
+    const int64_t r = st[--sp], l = st[--sp];
+    int64_t o = 0;
+    if (in.op == GVO_OP_ADD) o = l + r;
+    else if (in.op == GVO_OP_SUB) o = l - r;
+    else if (l != 0 || r != 0) return false;  // *, //, % of a base-carrying operand
+    if (o < -8 || o > 8) return false;
+    st[sp++] = o;
+  }
+  return sp == 1 && st[0] == 1;
+}
+
+static void put_bytes(std::string& k, const void* p, size_t n) { k.append(reinterpret_cast<const char*>(p), n); }
+
+// fclass[field_base_off[t] + f] and tclass[t]: equal ids <=> the same
+// accesses (kind, multiplicity, bytecode, in kernel order) up to the field
+// bases, every access translation-safe; -1 = never shared
+static void translation_classes(const gvo_template* t, int n, std::vector<int32_t>& fcls, std::vector<int32_t>& tcls) {
+  std::unordered_map<std::string, int32_t> fmap, tmap;
+  fcls.clear();
+  tcls.assign(n, -1);
+  for (int i = 0; i < n; ++i) {
+    const gvo_template& T = t[i];
+    bool all_ok = true;
+    for (int f = 0; f < T.n_fields; ++f) {
+      std::string key;
+      bool ok = true;
+      for (int a = 0; a < T.n_accesses && ok; ++a) {
+        if (T.access_field[a] != f) continue;
+        const gvo_insn* code = T.code + T.access_code_off[a];
+        const int len = T.access_code_len[a];
+        ok = base_additive(code, len, f);
+        put_bytes(key, &T.access_kind[a], 4);
+        put_bytes(key, &T.access_mult[a], 8);
+        put_bytes(key, &len, 4);
+        for (int k = 0; k < len; ++k) {
+          put_bytes(key, &code[k].op, 4);
+          const int64_t arg = code[k].op == GVO_OP_BASE ? -1 : code[k].arg;
+          put_bytes(key, &arg, 8);
+        }
+      }
+      int32_t id = -1;
+      if (ok) {
+        auto it = fmap.emplace(key, (int32_t)fmap.size()).first;
+        id = it->second;
+      }
+      fcls.push_back(id);
+      all_ok = all_ok && ok;
+    }
+    if (!all_ok) continue;
+    std::string key;
+    put_bytes(key, &T.n_fields, 4);
+    for (int a = 0; a < T.n_accesses; ++a) {
+      put_bytes(key, &T.access_field[a], 4);
+      put_bytes(key, &T.access_kind[a], 4);
+      put_bytes(key, &T.access_mult[a], 8);
+      const int len = T.access_code_len[a];
+      put_bytes(key, &len, 4);
+      for (int k = 0; k < len; ++k) {
+        const gvo_insn& in = T.code[T.access_code_off[a] + k];
+        put_bytes(key, &in.op, 4);
+        put_bytes(key, &in.arg, 8);
+      }
+    }
+    tcls[i] = tmap.emplace(key, (int32_t)tmap.size()).first->second;
+  }
+}
+
 extern "C" {
 
 int gvo_abi_version(void) { return GVO_ABI_VERSION; }
@@ -190,6 +286,7 @@ int gvo_open(int device, gvo_ctx** out) {
   if (const char* e = getenv("GVO_WAVE_ORDER")) ctx->wave_fm = atoi(e) != 0;
   if (const char* e = getenv("GVO_FUSE_WARP")) ctx->fuse_warp = atoi(e) != 0;
   if (const char* e = getenv("GVO_BIG_BATCH")) { ctx->big_batch = atoll(e); ctx->big_forced = true; }
+  if (const char* e = getenv("GVO_DEDUP")) ctx->dedup = atoi(e) != 0;
   ctx->n_ctas = kMaxSetsCtasPerSm * ctx->n_sm;
   *out = ctx;
   return GVO_OK;
@@ -203,6 +300,11 @@ void gvo_close(gvo_ctx* ctx) {
     b->release();
   ctx->t_fb.release();
   ctx->t_am.release();
+  ctx->t_fcls.release();
+  ctx->t_tcls.release();
+  ctx->d_mclass.release();
+  ctx->dd_table.release();
+  ctx->dd_lead.release();
   ctx->t_code.release();
   ctx->d_machines.release();
   ctx->coefs.release();
@@ -300,6 +402,12 @@ int gvo_set_templates(gvo_ctx* ctx, const gvo_template* t, int32_t n) {
   rc |= up32(ctx->t_af, af); rc |= up32(ctx->t_ak, ak); rc |= up32(ctx->t_co, co); rc |= up32(ctx->t_cl, cl);
   rc |= up32(ctx->t_fko, fko); rc |= up32(ctx->t_fkl, fkl);
   rc |= up64(ctx->t_fb, fb); rc |= up64(ctx->t_am, am);
+  {
+    std::vector<int32_t> fcls, tcls;
+    translation_classes(t, n, fcls, tcls);
+    rc |= up32(ctx->t_fcls, fcls);
+    rc |= up32(ctx->t_tcls, tcls);
+  }
   if (rc) return set_err(ctx, GVO_ERR_CUDA, "template upload failed%s");
   if (!ctx->t_code.ensure(std::max<size_t>(code.size(), 1))) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
   CK(cudaMemcpy(ctx->t_code.p, code.data(), code.size() * sizeof(gvo_insn), cudaMemcpyHostToDevice));
@@ -316,6 +424,7 @@ int gvo_set_templates(gvo_ctx* ctx, const gvo_template* t, int32_t n) {
   V.field_base = ctx->t_fb.p; V.acc_field = ctx->t_af.p; V.acc_kind = ctx->t_ak.p; V.acc_mult = ctx->t_am.p;
   V.code_off = ctx->t_co.p; V.code_len = ctx->t_cl.p; V.code = ctx->t_code.p;
   V.fk_off = ctx->t_fko.p; V.fk_list = ctx->t_fkl.p; V.max_acc = maxa;
+  V.fclass = ctx->t_fcls.p; V.tclass = ctx->t_tcls.p;
   // pageable cudaMemcpy may return before its DMA lands, and the pipeline
   // runs on non-blocking streams: make the upload visible to every stream
   CK(cudaDeviceSynchronize());
@@ -333,6 +442,27 @@ int gvo_set_machines(gvo_ctx* ctx, const gvo_machine* m, int32_t n) {
   ctx->h_machines.assign(m, m + n);
   if (!ctx->d_machines.ensure(n)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
   CK(cudaMemcpy(ctx->d_machines.p, m, n * sizeof(gvo_machine), cudaMemcpyHostToDevice));
+  // machine classes: the integer parameters the set problems depend on
+  // (granules, banks, waves); capacities, bandwidths, clock and fits only
+  // enter the float assembly
+  {
+    std::vector<int32_t> mc(n);
+    for (int i = 0; i < n; ++i) {
+      mc[i] = i;
+      for (int k = 0; k < i; ++k) {
+        const gvo_machine &a = m[i], &b = m[k];
+        if (a.sm_count == b.sm_count && a.l1_line_bytes == b.l1_line_bytes && a.sector_bytes == b.sector_bytes &&
+            a.l1_banks == b.l1_banks && a.bank_width_bytes == b.bank_width_bytes &&
+            a.max_threads_per_sm == b.max_threads_per_sm && a.max_blocks_per_sm == b.max_blocks_per_sm &&
+            a.max_threads_per_block == b.max_threads_per_block) {
+          mc[i] = mc[k];
+          break;
+        }
+      }
+    }
+    if (!ctx->d_mclass.ensure(n)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
+    CK(cudaMemcpy(ctx->d_mclass.p, mc.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
   CK(cudaDeviceSynchronize());
   return GVO_OK;
 }
@@ -345,6 +475,9 @@ static int ensure_work(gvo_ctx* ctx, int64_t n) {
     ctx->slab_bytes = sets_slab_bytes(ctx->run_cap, ctx->elem_cap);
     if (!ctx->slab.ensure((size_t)ctx->slab_bytes * ctx->n_ctas))
       return set_err(ctx, GVO_ERR_CUDA, "scratch slab alloc failed%s");
+    // run records are copied whole (descriptor arena) although a run kind
+    // leaves some fields unused: defined bytes for initcheck, once
+    CK(cudaMemset(ctx->slab.p, 0, (size_t)ctx->slab_bytes * ctx->n_ctas));
   }
   if (!ctx->status.ensure(4) || !ctx->work.ensure(1)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
   if (!ctx->split) {
@@ -393,6 +526,25 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
   sampling_eff(sampling, &S, &W);
   const int64_t stride = gvo_counts_stride(F, S, W);
   const gvo_machine& m0 = ctx->h_machines[0];
+  // one sharing table per call (k_dedup.cu): keys of every batch, so later
+  // batches reuse earlier batches' counts
+  const bool dedup = ctx->dedup && n > 0 && ctx->t_fcls.p && ctx->d_mclass.p;
+  if (dedup) {
+    const int64_t want = 2 * dedup_units(n, F, S);
+    int64_t cap = int64_t(1) << 12;
+    while (cap < want && cap < (int64_t(1) << 23)) cap <<= 1;
+    if (!ctx->dd_table.ensure((size_t)cap + 1) || !ctx->status.ensure(4))
+      return set_err(ctx, GVO_ERR_CUDA, "sharing table alloc failed%s");
+    ctx->dd_mask = cap - 1;
+    CK(cudaMemsetAsync(ctx->dd_table.p, 0, (size_t)cap * sizeof(DedupEntry), st));
+  }
+  ctx->dd_units = ctx->dd_follow = 0;
+  unsigned long long* dd_stats = nullptr;
+  if (dedup && ctx->dd_count) {
+    if (!ctx->work.ensure(4)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
+    dd_stats = ctx->work.p + 2;
+    CK(cudaMemsetAsync(dd_stats, 0, 2 * sizeof(unsigned long long), st));
+  }
   for (int64_t b0 = 0; b0 < n; b0 += ctx->batch) {
     const int64_t nb = std::min(ctx->batch, n - b0);
     int rc = ensure_work(ctx, nb);
@@ -404,12 +556,20 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     cudaEvent_t tb = nullptr;
     tmark_begin(ctx, 0, st, &tb);
     launch_setup(ctx->view, ctx->d_machines.p, cf, nb, *sampling, ctx->coefs.p, ctx->geos.p, ctx->ctabs.p, st);
+    int64_t* lead = nullptr;
+    if (dedup) {
+      if (!ctx->dd_lead.ensure((size_t)dedup_units(nb, F, S))) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
+      lead = ctx->dd_lead.p;
+      launch_dedup(ctx->view, ctx->d_machines.p, ctx->d_mclass.p, cf, ctx->geos.p, nb, F, S, b0, ctx->dd_table.p,
+                   ctx->dd_mask, lead, dd_stats, st);
+    }
     tmark_end(ctx, 0, st, tb);
     // warp statistics: fused into the k_sets work queue when their shared
     // memory fits the set kernel's element buffer, else a separate launch
     WarpArgs WA{ctx->view, ctx->d_machines.p, cf, ctx->geos.p, ctx->coefs.p, nb * (S + 1), S, m0.sector_bytes,
                m0.bank_width_bytes, m0.l1_banks, 0, nullptr, cnt, stride, F,
-               d_l1_access ? d_l1_access + b0 * l1_stride * 3 : nullptr, l1_stride, nullptr};
+               d_l1_access ? d_l1_access + b0 * l1_stride * 3 : nullptr, l1_stride, nullptr,
+               lead ? lead + nb * F * (S + 1) : nullptr};
     const bool big = nb >= ctx->big_batch && (ctx->big_forced || ctx->all_wide);
     const bool fuse = ctx->fuse_warp &&
                       (int64_t)warp_item_smem(ctx->max_acc) <= (big ? sets1::sets_ebuf_bytes() : sets2::sets_ebuf_bytes());
@@ -446,6 +606,7 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     L.seg_off = ctx->seg_off;
     L.pat_off = ctx->pat_off;
     L.wave_field_major = ctx->wave_fm;
+    L.lead = lead;
     if (fuse) {
       L.warp = WA;
       L.n_warp_items = WA.n_items;
@@ -465,6 +626,8 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     } else {
       sets2::launch_sets(L, st);
     }
+    if (lead)
+      launch_dedup_copy(cf, ctx->geos.p, ctx->view, d_counts, stride, nb, F, S, b0, lead, d_l1_access, l1_stride, st);
     tmark_end(ctx, 2, st, tb);
     tmark_begin(ctx, 3, st, &tb);
     launch_finish(ctx->view, ctx->d_machines.p, cf, ctx->geos.p, nb, S, W, F, cnt, stride,
@@ -473,6 +636,27 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     tmark_end(ctx, 3, st, tb);
     CK(cudaGetLastError());
   }
+  if (dd_stats) {
+    unsigned long long h[2] = {0, 0};
+    CK(cudaMemcpyAsync(h, dd_stats, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ctx->dd_units = (int64_t)h[0];
+    ctx->dd_follow = (int64_t)h[1];
+  }
+  return GVO_OK;
+}
+
+int gvo_dedup_stats(gvo_ctx* ctx, int enable_counting, int64_t* shareable_units, int64_t* followers) {
+  if (!ctx) return GVO_ERR_INVALID;
+  ctx->dd_count = enable_counting != 0;
+  if (shareable_units) *shareable_units = ctx->dd_units;
+  if (followers) *followers = ctx->dd_follow;
+  return ctx->dedup ? 1 : 0;
+}
+
+int gvo_set_dedup(gvo_ctx* ctx, int enable) {
+  if (!ctx) return GVO_ERR_INVALID;
+  ctx->dedup = enable != 0;
   return GVO_OK;
 }
 

@@ -77,6 +77,10 @@ struct TplView {
   const int32_t* fk_off;   // [n_tpl][2*kMaxFields+1]
   const int32_t* fk_list;  // global access index (within template) lists
   int32_t max_acc;         // max accesses over templates (coef row stride)
+  // translation classes for cross-config sharing (k_dedup.cu; host-built in
+  // capi.cu): fclass[field_base_off[t] + f] / tclass[t], -1 = never shared
+  const int32_t* fclass;
+  const int32_t* tclass;
 };
 
 // ---------------------------------------------------------------- classes

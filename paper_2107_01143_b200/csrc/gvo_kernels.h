@@ -62,6 +62,7 @@ struct SetsLaunch {
   int32_t pat_off = 0;
   int32_t wave_field_major = 1;
   int32_t epoch = 1;  // launch number, unique across both residencies (queue readiness tag)
+  const int64_t* lead = nullptr;  // k_dedup: >= 0 = unit copied from another config's (skip)
 };
 namespace sets1 {
 int64_t sets_ebuf_bytes();
@@ -73,6 +74,22 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st);
 }
 int64_t sets_slab_bytes(int64_t run_cap, int64_t elem_cap);
 int64_t split_slot_bytes(int64_t run_cap);
+
+// cross-configuration sharing of identical set problems (k_dedup.cu)
+struct DedupEntry {
+  unsigned long long tag;  // 0 empty, else key hash | 1
+  int64_t leader;          // global config index * 32 + field
+  int ready;
+  int pad;
+  uint64_t key[9];
+};
+int64_t dedup_units(int64_t n, int F, int S);
+void launch_dedup(const TplView& T, const gvo_machine* d_machines, const int32_t* d_mclass, const gvo_config* d_cfgs,
+                  const Geo* d_geos, int64_t n, int F, int S, int64_t b0, DedupEntry* table, int64_t mask,
+                  int64_t* d_lead, unsigned long long* d_stats, cudaStream_t st);
+void launch_dedup_copy(const gvo_config* d_cfgs, const Geo* d_geos, const TplView& T, int64_t* d_counts_all,
+                       int64_t counts_stride, int64_t n, int F, int S, int64_t b0, const int64_t* d_lead,
+                       int64_t* d_l1_access_all, int32_t l1_stride, cudaStream_t st);
 
 // float assembly + prediction (k_assemble.cu)
 void launch_finish(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs,

@@ -64,6 +64,7 @@ struct WarpArgs {
   int64_t* l1_access;
   int32_t l1_stride;
   unsigned long long* out_totals;
+  const int64_t* lead;  // mode 0: k_dedup marks, indexed by item (>= 0: copied, skip); may be null
 };
 
 constexpr int kWarpDedupAcc = 256;   // grouping is quadratic in the access count: off beyond
@@ -104,6 +105,7 @@ static __device__ __noinline__ void warp_item(const WarpArgs& W, int64_t item, u
       j = (int)(item % (S_req + 1));
       const Geo& G = geos[c];
       is_l1 = j == S_req;
+      if (W.lead && W.lead[item] >= 0) return;  // counts copied from an identical item (k_dedup.cu)
       if (!phase_ok(G, is_l1 ? 2 : 0)) return;
       if (!is_l1 && j >= G.n_samples) return;
       blk = is_l1 ? G.l1_block : G.sample_lin[j];
@@ -303,7 +305,7 @@ static __device__ __noinline__ void warp_item(const WarpArgs& W, int64_t item, u
     // group members take their representative's per-access L1 numbers
     if (is_l1)
       for (int a = threadIdx.x; a < A; a += blockDim.x)
-        if (rep[a] >= 0) {
+        if (rep[a] >= 0 && rep[a] != a) {
           const int r = rep[a];  // the representative's access index
           acc_l1[3 * a + 0] = acc_l1[3 * r + 0];
           acc_l1[3 * a + 1] = acc_l1[3 * r + 1];

@@ -1883,6 +1883,7 @@ struct SetsArgs {
   int32_t pat_off;          // A/B hook: no pattern runs
   int32_t wave_field_major; // wave units ordered field-major (heavy fields first)
   int32_t epoch;            // launch number; queue slots are ready when ready == epoch
+  const int64_t* lead;      // mode 0, k_dedup.cu: >= 0 = unit copied from an identical one (skip); may be null
 };
 
 // ------------------------------------------------------------------ micro tier
@@ -1936,6 +1937,7 @@ __device__ bool micro_unit(const SetsArgs& P, int64_t bidx, uint8_t* reg, int64_
   const gvo_config cfg = P.cfgs[c];
   const int tpl = cfg.template_id;
   if (f >= P.T.n_fields[tpl] || !phase_ok(G, 0) || j >= G.n_samples || G.dup_of[f][j] >= 0) return true;
+  if (P.lead && P.lead[(int64_t)F * (P.n_items / ((int64_t)F * (S + 1))) + bidx] >= 0) return true;
   MicroCnt* cnt = reinterpret_cast<MicroCnt*>(reg);
   int64_t* roff = reinterpret_cast<int64_t*>(reg + ((sizeof(MicroCnt) + 15) & ~size_t(15)));
   uint64_t* el = reinterpret_cast<uint64_t*>(roff + kMicroRuns + 1);
@@ -2339,6 +2341,10 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         const gvo_config& cfg = P.cfgs[c];
         if (f >= P.T.n_fields[cfg.template_id]) skip = true;
         if (P.mode == 0 && !phase_ok(G, j < P.S_req ? 0 : 1)) skip = true;
+        // identical unit of another configuration (k_dedup.cu): copied after the launch
+        if (P.mode == 0 && P.lead && !skip &&
+            P.lead[j < P.S_req ? n_wave_u + (c * P.F_stride + f) * P.S_req + j : c * P.F_stride + f] >= 0)
+          skip = true;
         U.cfg = c;
         U.field = (int)f;
         U.j = j;
@@ -3161,6 +3167,7 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st) {
   P.sm_cap = L.sm_cap;
   P.seg_off = L.seg_off;
   P.pat_off = L.pat_off;
+  P.lead = L.lead;
   P.wave_field_major = L.wave_field_major;
   P.epoch = L.epoch;  // never 0 (the zeroed initial state), unique per launch
   if (P.n_items + P.n_warp_items <= 0) return;
