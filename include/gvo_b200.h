@@ -357,7 +357,10 @@ int gvo_debug_units(gvo_ctx* ctx, int enable, int64_t* h_out, int64_t cap, int64
  * is on, 0 when off.  (No reference counterpart: the reference evaluates every
  * configuration from scratch, perf.py:115-130; results are identical.) */
 int gvo_dedup_stats(gvo_ctx* ctx, int enable_counting, int64_t* shareable_units, int64_t* followers);
-/* Turn the sharing on (1) or off (0) for later calls on this context. */
+/* Turn the sharing on (1) or off (0) for later calls on this context: both
+ * the set-problem sharing above and the plan sharing of k_setup (leader plans
+ * of configurations equal up to field-base translation and machine
+ * capacities; GVO_PLAN_SHARE=0 turns that one off alone). */
 int gvo_set_dedup(gvo_ctx* ctx, int enable);
 /* Measured INT32 issue rate of the device (ops/s), the integer roofline. */
 int gvo_int_peak(gvo_ctx* ctx, double* ops_per_s);

@@ -88,6 +88,12 @@ struct gvo_ctx {
   // cross-configuration sharing of identical set problems (k_dedup.cu):
   // GVO_DEDUP=0 evaluates every unit of every configuration
   bool dedup = true;
+  // plan sharing across configurations (k_setup.cu): key table, leader
+  // plan cache and per-batch sources, one table per call
+  bool plan_share = true;
+  DBuf<PlanEntry> plan_table;
+  DBuf<int64_t> plan_cache, plan_src;
+  DBuf<unsigned long long> plan_used;
   DBuf<DedupEntry> dd_table;
   int64_t dd_mask = 0;
   DBuf<int64_t> dd_lead;
@@ -287,6 +293,7 @@ int gvo_open(int device, gvo_ctx** out) {
   if (const char* e = getenv("GVO_FUSE_WARP")) ctx->fuse_warp = atoi(e) != 0;
   if (const char* e = getenv("GVO_BIG_BATCH")) { ctx->big_batch = atoll(e); ctx->big_forced = true; }
   if (const char* e = getenv("GVO_DEDUP")) ctx->dedup = atoi(e) != 0;
+  if (const char* e = getenv("GVO_PLAN_SHARE")) ctx->plan_share = atoi(e) != 0;
   ctx->n_ctas = kMaxSetsCtasPerSm * ctx->n_sm;
   *out = ctx;
   return GVO_OK;
@@ -304,11 +311,19 @@ void gvo_close(gvo_ctx* ctx) {
   ctx->t_tcls.release();
   ctx->d_mclass.release();
   ctx->dd_table.release();
+  ctx->plan_table.release();
+  ctx->plan_cache.release();
+  ctx->plan_src.release();
+  ctx->plan_used.release();
   ctx->dd_lead.release();
   ctx->t_code.release();
   ctx->d_machines.release();
   ctx->coefs.release();
+  ctx->ctabs.release();
   ctx->geos.release();
+  ctx->work.release();
+  ctx->s_order.release();
+  ctx->unit_stats.release();
   ctx->slab.release();
   ctx->status.release();
   ctx->split_mem.release();
@@ -538,6 +553,25 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     ctx->dd_mask = cap - 1;
     CK(cudaMemsetAsync(ctx->dd_table.p, 0, (size_t)cap * sizeof(DedupEntry), st));
   }
+  // plan sharing: one key table and leader-plan cache per call
+  PlanShare PS{};
+  if (ctx->plan_share && n > 1 && ctx->d_mclass.p) {
+    int64_t cap = int64_t(1) << 10;
+    while (cap < 2 * n && cap < (int64_t(1) << 22)) cap <<= 1;
+    const int64_t words = plan_slot_words(ctx->max_acc);
+    const int64_t slots = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t(512) << 20) / (words * 8)));
+    if (!ctx->plan_table.ensure((size_t)cap) || !ctx->plan_cache.ensure((size_t)(slots * words)) ||
+        !ctx->plan_used.ensure(1) || !ctx->plan_src.ensure((size_t)std::min(n, ctx->batch)))
+      return set_err(ctx, GVO_ERR_CUDA, "plan sharing alloc failed%s");
+    CK(cudaMemsetAsync(ctx->plan_table.p, 0, (size_t)cap * sizeof(PlanEntry), st));
+    CK(cudaMemsetAsync(ctx->plan_used.p, 0, sizeof(unsigned long long), st));
+    PS.table = ctx->plan_table.p;
+    PS.mask = cap - 1;
+    PS.cache = ctx->plan_cache.p;
+    PS.cap = slots;
+    PS.n_used = ctx->plan_used.p;
+    PS.src = ctx->plan_src.p;
+  }
   ctx->dd_units = ctx->dd_follow = 0;
   unsigned long long* dd_stats = nullptr;
   if (dedup && ctx->dd_count) {
@@ -555,7 +589,8 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     CK(cudaMemsetAsync(cnt, 0, (size_t)nb * stride * 8, st));
     cudaEvent_t tb = nullptr;
     tmark_begin(ctx, 0, st, &tb);
-    launch_setup(ctx->view, ctx->d_machines.p, cf, nb, *sampling, ctx->coefs.p, ctx->geos.p, ctx->ctabs.p, st);
+    launch_setup(ctx->view, ctx->d_machines.p, cf, nb, *sampling, ctx->coefs.p, ctx->geos.p, ctx->ctabs.p, st,
+                 ctx->d_mclass.p, PS.table ? &PS : nullptr);
     int64_t* lead = nullptr;
     if (dedup) {
       if (!ctx->dd_lead.ensure((size_t)dedup_units(nb, F, S))) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
@@ -657,6 +692,7 @@ int gvo_dedup_stats(gvo_ctx* ctx, int enable_counting, int64_t* shareable_units,
 int gvo_set_dedup(gvo_ctx* ctx, int enable) {
   if (!ctx) return GVO_ERR_INVALID;
   ctx->dedup = enable != 0;
+  ctx->plan_share = enable != 0;
   return GVO_OK;
 }
 

@@ -22,10 +22,17 @@ struct AffineForm {
 // Returns kAffine or kNonAffine.  Coefficients are exact: any intermediate
 // that leaves int64 downgrades the access to the per-point evaluator, which
 // is exact whenever the bounds check passed (all subexpressions in range).
+// *mag (optional) receives the largest |coefficient| of any node, or
+// UINT64_MAX when an intermediate left int64 (plan sharing, k_setup.cu).
 __device__ inline int affine_extract(const gvo_insn* code, int len, const int32_t bd[3],
-                                     const int64_t* field_base, AffineForm* out) {
+                                     const int64_t* field_base, AffineForm* out, uint64_t* mag = nullptr) {
   AffineForm st[kStack];
   int sp = 0;
+  uint64_t mx = 0;
+  auto amax = [&](int64_t v) {
+    const uint64_t a = v < 0 ? (uint64_t)0 - (uint64_t)v : (uint64_t)v;
+    if (a > mx) mx = a;
+  };
   for (int i = 0; i < len; ++i) {
     const gvo_insn in = code[i];
     if (in.op <= GVO_OP_BASE) {
@@ -37,6 +44,7 @@ __device__ inline int affine_extract(const gvo_insn* code, int len, const int32_
       else if (in.op == GVO_OP_COORD) f.c[1 + in.arg] = 1;
       else if (in.op == GVO_OP_BDIM) f.c[0] = bd[in.arg];
       else f.c[0] = field_base[in.arg];
+      amax(f.c[0]);
       st[sp++] = f;
       continue;
     }
@@ -48,8 +56,9 @@ __device__ inline int affine_extract(const gvo_insn* code, int len, const int32_
     if (in.op == GVO_OP_ADD || in.op == GVO_OP_SUB) {
       for (int k = 0; k < 7; ++k) {
         __int128 v = in.op == GVO_OP_ADD ? (__int128)l.c[k] + r.c[k] : (__int128)l.c[k] - r.c[k];
-        if (!fits_i64(v)) return kNonAffine;
+        if (!fits_i64(v)) { if (mag) *mag = ~0ull; return kNonAffine; }
         o.c[k] = (int64_t)v;
+        amax(o.c[k]);
       }
     } else {  // MUL: one side must be coordinate-free
       bool lconst = true, rconst = true;
@@ -62,14 +71,16 @@ __device__ inline int affine_extract(const gvo_insn* code, int len, const int32_
       const int64_t m = lconst ? l.c[0] : r.c[0];
       for (int k = 0; k < 7; ++k) {
         __int128 v = (__int128)s.c[k] * m;
-        if (!fits_i64(v)) return kNonAffine;
+        if (!fits_i64(v)) { if (mag) *mag = ~0ull; return kNonAffine; }
         o.c[k] = (int64_t)v;
+        amax(o.c[k]);
       }
     }
     st[sp++] = o;
   }
   if (sp != 1) return kNonAffine;
   *out = st[0];
+  if (mag) *mag = mx;
   return kAffine;
 }
 
@@ -105,12 +116,14 @@ __device__ inline int64_t eval_point(const gvo_insn* code, int len, const int64_
 // recursion order).  Returns -1 when all nodes stay in int64, else the
 // instruction index of the first failing node.  lo/hi receive the root
 // interval on success.
+// *mag (optional) receives the largest |bound| of any BinOp node.
 __device__ inline int bounds_check(const gvo_insn* code, int len, const int64_t clo[6],
                                    const int64_t chi[6], const int32_t bd[3],
                                    const int64_t* field_base, int64_t* root_lo,
-                                   int64_t* root_hi) {
+                                   int64_t* root_hi, uint64_t* mag = nullptr) {
   int64_t slo[kStack], shi[kStack];
   int sp = 0;
+  uint64_t mx = 0;
   for (int i = 0; i < len; ++i) {
     const gvo_insn in = code[i];
     if (in.op <= GVO_OP_BASE) {
@@ -148,9 +161,13 @@ __device__ inline int bounds_check(const gvo_insn* code, int len, const int64_t 
     slo[sp] = (int64_t)lo;
     shi[sp] = (int64_t)hi;
     ++sp;
+    const uint64_t alo = lo < 0 ? (uint64_t)(-lo) : (uint64_t)lo, ahi = hi < 0 ? (uint64_t)(-hi) : (uint64_t)hi;
+    if (alo > mx) mx = alo;
+    if (ahi > mx) mx = ahi;
   }
   *root_lo = slo[0];
   *root_hi = shi[0];
+  if (mag) *mag = mx;
   return -1;
 }
 

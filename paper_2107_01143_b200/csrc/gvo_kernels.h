@@ -17,9 +17,26 @@ constexpr int kMaxSetsCtasPerSm = GVO_SETS2_CTAS;
 constexpr int kMaxSetsCtasPerSm = 2;
 #endif
 
+// plan sharing across configurations (k_setup.cu): a per-call key table
+// and a cache of leader plans
+struct PlanEntry {
+  unsigned long long tag;  // 0 empty, else key hash | 1
+  int ready;
+  int slot;                // cache slot, -1 = cache full
+  uint64_t key[6];
+};
+struct PlanShare {
+  PlanEntry* table = nullptr;
+  int64_t mask = 0;
+  int64_t* cache = nullptr;      // cap slots of plan_slot_words(max_acc) int64
+  int64_t cap = 0;
+  unsigned long long* n_used = nullptr;
+  int64_t* src = nullptr;        // per batch config: slot, -2 - slot (leader) or -1
+};
+__host__ __device__ int64_t plan_slot_words(int64_t max_acc);
 void launch_setup(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs,
                   int64_t n, const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos, int64_t* d_ctabs,
-                  cudaStream_t st);
+                  cudaStream_t st, const int32_t* d_mclass = nullptr, const PlanShare* share = nullptr);
 void launch_classes(const TplView& T, const gvo_config* d_cfgs, int64_t n, const int64_t* d_coefs,
                     int64_t* d_ctabs, cudaStream_t st);
 

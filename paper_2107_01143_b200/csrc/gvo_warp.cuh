@@ -76,6 +76,14 @@ __host__ __device__ inline size_t warp_item_smem(int max_acc) {
 }
 
 // One item, all threads of the CTA (blockDim.x multiple of 32).
+#if defined(GVO_DEBUG_SYNC) && GVO_DEBUG_SYNC
+// debug build: which exit each warp took (0 not run, 1 all fields copied, 2 end)
+__shared__ int gvo_dbg_wexit[3];
+#define GVO_DBG_WEXIT(k) do { if ((threadIdx.x & 31) == 0) atomicAdd(&gvo_dbg_wexit[k], 1); } while (0)
+#else
+#define GVO_DBG_WEXIT(k) do { } while (0)
+#endif
+
 static __device__ __noinline__ void warp_item(const WarpArgs& W, int64_t item, unsigned long long* sh) {
   const TplView& T = W.T;
   const gvo_machine* machines = W.machines;
@@ -105,10 +113,19 @@ static __device__ __noinline__ void warp_item(const WarpArgs& W, int64_t item, u
       j = (int)(item % (S_req + 1));
       const Geo& G = geos[c];
       is_l1 = j == S_req;
-      if (W.lead && W.lead[item] >= 0) return;  // counts copied from an identical item (k_dedup.cu)
-      if (!phase_ok(G, is_l1 ? 2 : 0)) return;
-      if (!is_l1 && j >= G.n_samples) return;
-      blk = is_l1 ? G.l1_block : G.sample_lin[j];
+      // whether the item runs is decided once, by thread 0, and broadcast:
+      // every thread takes the same path to the barriers below
+      __shared__ int s_run;
+      __shared__ int64_t s_blk;
+      if (threadIdx.x == 0) {
+        bool run = !(W.lead && W.lead[item] >= 0);  // else counts copied from an identical item (k_dedup.cu)
+        run = run && phase_ok(G, is_l1 ? 2 : 0) && (is_l1 || j < G.n_samples);
+        s_run = run;
+        s_blk = run ? (is_l1 ? G.l1_block : G.sample_lin[j]) : 0;
+      }
+      __syncthreads();
+      if (!s_run) { GVO_DBG_WEXIT(0); return; }
+      blk = s_blk;
     } else {
       c = 0;
       blk = block_list[item];
@@ -145,17 +162,24 @@ static __device__ __noinline__ void warp_item(const WarpArgs& W, int64_t item, u
     int32_t* keys = rep + A;                                 // representatives in access order
     int32_t* kidx = keys + A;                                // key index of a representative
     const bool dedup = A <= kWarpDedupAcc;
-    uint32_t skip_field = 0;  // fields whose sample is a translate of an earlier one
-    if (mode == 0 && !is_l1)
-      for (int f = 0; f < kMaxFields; ++f) skip_field |= (geos[c].dup_of[f][j] >= 0 ? 1u : 0u) << f;
+    // fields whose sample is a translate of an earlier one (thread 0 reads
+    // the plan, the CTA shares the mask)
+    __shared__ uint32_t s_skip;
+    if (threadIdx.x == 0) {
+      uint32_t m = 0;
+      if (mode == 0 && !is_l1)
+        for (int f = 0; f < kMaxFields; ++f) m |= (geos[c].dup_of[f][j] >= 0 ? 1u : 0u) << f;
+      s_skip = m;
+    }
+    __syncthreads();
+    const uint32_t skip_field = s_skip;
     // every field of this sample is a translate of an earlier sample: k_finish
     // copies all its counts, nothing to evaluate (uniform across the CTA)
     {
       const int nf = T.n_fields[tpl];
       const uint32_t all = nf >= 32 ? ~0u : ((1u << nf) - 1u);
-      if (mode == 0 && !is_l1 && nf > 0 && (skip_field & all) == all) return;
+      if (mode == 0 && !is_l1 && nf > 0 && (skip_field & all) == all) { GVO_DBG_WEXIT(1); return; }
     }
-    __syncthreads();
     // group of each access: first access of the same field, kind and
     // coefficients whose constant (block terms included) has the same residue
     const int64_t modulus = is_l1 ? bw * nbk : sec;
@@ -344,6 +368,7 @@ static __device__ __noinline__ void warp_item(const WarpArgs& W, int64_t item, u
         for (int k = 0; k < 3; ++k) out_totals[3 * a + k] = acc_l1[3 * a + k];
     }
     __syncthreads();
+    GVO_DBG_WEXIT(2);
   
   }
 }

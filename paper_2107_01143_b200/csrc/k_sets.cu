@@ -22,6 +22,9 @@
 #include "gvo_bytecode.cuh"
 #include "gvo_kernels.h"
 #include "gvo_warp.cuh"
+#if defined(GVO_DEBUG_SYNC) && GVO_DEBUG_SYNC
+#include <cstdio>
+#endif
 
 // residency of this build of the set kernel (k_sets1.cu includes this file
 // with 1); each residency lives in its own namespace
@@ -2173,7 +2176,17 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
   const int64_t n_main = n_set_main + P.n_warp_items;
   const int64_t kBlkBase = int64_t(1) << 40;
 
+#if defined(GVO_DEBUG_SYNC) && GVO_DEBUG_SYNC
+  // debug build: every warp counts its passes through the item loop; after
+  // the fetch barrier thread 0 checks that all warps are on the same pass
+  __shared__ int dbg_iter[kNW];
+  if ((threadIdx.x & 31) == 0) dbg_iter[threadIdx.x >> 5] = 0;
+  __syncthreads();
+#endif
   for (;;) {
+#if defined(GVO_DEBUG_SYNC) && GVO_DEBUG_SYNC
+    if ((threadIdx.x & 31) == 0) dbg_iter[threadIdx.x >> 5] += 1;
+#endif
     // ---------------- fetch: queued key ranges first, then main items
     const long long t_fetch = clock64();
     if (threadIdx.x == 0) {
@@ -2243,6 +2256,16 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
     __syncthreads();
     const int kind_fetched = next_kind;
     const int64_t item = next_item;
+#if defined(GVO_DEBUG_SYNC) && GVO_DEBUG_SYNC
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < kNW; ++w)
+        if (dbg_iter[w] != dbg_iter[0]) {
+          printf("GVO_DEBUG_SYNC block %d: warp %d on pass %d, warp 0 on pass %d (kind %d item %lld)\n", blockIdx.x, w,
+                 dbg_iter[w], dbg_iter[0], kind_fetched, (long long)item);
+          break;
+        }
+    }
+#endif
     GVO_PH(if (threadIdx.x == 0) ph[0] += clock64() - t_fetch;)
     if (kind_fetched == 2) break;
 
@@ -2252,8 +2275,18 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
     const long long t_start = clock64();
 
     if (!in_range && item >= n_set_main && item < kBlkBase) {
+#if defined(GVO_DEBUG_SYNC) && GVO_DEBUG_SYNC
+      if (threadIdx.x < 3) gvo_dbg_wexit[threadIdx.x] = 0;
+      __syncthreads();
+#endif
       warp_item(P.warp, item - n_set_main, reinterpret_cast<unsigned long long*>(ebuf));
       __syncthreads();
+#if defined(GVO_DEBUG_SYNC) && GVO_DEBUG_SYNC
+      if (threadIdx.x == 0 && gvo_dbg_wexit[0] != kNW && gvo_dbg_wexit[1] != kNW && gvo_dbg_wexit[2] != kNW)
+        printf("GVO_DEBUG_SYNC block %d: warp item %lld exits %d/%d/%d\n", blockIdx.x, (long long)(item - n_set_main),
+               gvo_dbg_wexit[0], gvo_dbg_wexit[1], gvo_dbg_wexit[2]);
+      __syncthreads();
+#endif
       GVO_PH(if (threadIdx.x == 0) ph[1] += clock64() - t_start;)
       if (threadIdx.x == 0 && SS) atomicAdd(&SS->pending, ~0ull);
       continue;
@@ -2730,9 +2763,13 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         bm_r_ok = bm_r_ok && U.sub_r[q] >= 1 && U.sub_r[q] <= 32 && (32 % U.sub_r[q]) == 0;
       const int64_t bm_words = sm_elems * 4;  // ebuf holds 2*sm_elems 8-byte elements
       const bool has_pat = *reinterpret_cast<volatile const int32_t*>(&hdr->has_pattern) != 0;
+      // reset here and at the end of every pass that continues (by thread
+      // 0, before the pass's last barrier): the loop-exit read of s_split
+      // is a vector load that also covers s_nonmono, so a reset at the top
+      // of the loop would race with it
+      if (threadIdx.x == 0) { s_nonmono = 0; s_rtags = 0u; }
       for (;;) {
         // count in-range elements per run (monotone runs: closed form)
-        if (threadIdx.x == 0) { s_nonmono = 0; s_rtags = 0u; }
         __syncthreads();
         uint32_t my_tags = 0;  // tags of the runs with elements in [a, b)
         for (int r = threadIdx.x; r < nr; r += kNT) {
@@ -2870,6 +2907,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           cur_range.a = a;
           cur_range.b = b;
         }
+        if (threadIdx.x == 0 && s_split) { s_nonmono = 0; s_rtags = 0u; }  // the next pass's
         __syncthreads();
         b = cur_range.b;
         if (!s_split) break;

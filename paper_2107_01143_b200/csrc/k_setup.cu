@@ -205,15 +205,105 @@ __device__ __forceinline__ unsigned long long fail_key(int phase, int gorder, in
          ((unsigned long long)(f * 2 + kind) << 16) | (unsigned long long)a;
 }
 
-// One CTA per configuration.
-__global__ void __launch_bounds__(256) k_setup(TplView T, const gvo_machine* machines, const gvo_config* cfgs,
-                                               int64_t n, gvo_sampling smp, int64_t* coefs, Geo* geos,
-                                               int64_t* ctabs) {
+// ------------------------------------------------------------------ plan sharing
+// The plan of a configuration (coefficients, classes, geometry, overflow
+// guard) depends only on its template's accesses, the launch and the
+// machine's integer parameters — not on capacities, bandwidths or fits, and,
+// for translation-safe templates (capi.cu translation_classes: every field
+// base enters its accesses additively with coefficient 1), on the field
+// bases only through a shift: moving base_f by D moves the constant of
+// every affine access of field f, and every node interval of the guard,
+// by o*D with |o| <= 8 (o = the node's base coefficient).  So one leader per
+// key (translation class, block, grid, work per thread, machine class)
+// computes the plan, and its followers take it with the constants shifted.
+// Exactness: the leader's plan is shared only if its status is OK and every
+// coefficient and every guard interval bound of every node is <= 2^62 in
+// magnitude; a follower with |D| <= 2^58 then has every node within
+// 2^62 + 8*2^58 < 2^63 - 1: the same affine flags and no overflow, which
+// is what the reference computes for it.  Anything else computes itself.
+// The reference recomputes every configuration (perf.py:115-130).
+namespace {
+constexpr int kPlanKey = 6;
+constexpr int kPlanProbe = 64;
+constexpr uint64_t kPlanMag = uint64_t(1) << 62;
+constexpr int64_t kPlanShift = int64_t(1) << 58;
+
+__device__ __forceinline__ uint64_t pmix(uint64_t h, uint64_t v) {
+  h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  h *= 0xff51afd7ed558ccdull;
+  return h ^ (h >> 29);
+}
+
+// cache slot layout (int64 words): [0] share_ok, [1, 1+F) leader field
+// bases, then Geo, the coefficient row and the class table row
+__host__ __device__ inline int64_t plan_geo_off() { return (1 + kMaxFields + 1) & ~int64_t(1); }
+__host__ __device__ inline int64_t plan_coef_off() { return plan_geo_off() + ((int64_t)sizeof(Geo) + 15) / 16 * 2; }
+__host__ __device__ inline int64_t plan_ctab_off(int64_t A) { return plan_coef_off() + A * 8; }
+}  // namespace
+
+__host__ __device__ int64_t plan_slot_words(int64_t max_acc) { return plan_ctab_off(max_acc) + ctab_stride(max_acc); }
+
+// One thread per configuration of the batch: src[c] = slot >= 0 (take the
+// plan cached in slot), -2 - slot (leader: compute, then fill slot), -1
+// (compute, not shared).
+__global__ void k_plan_key(TplView T, const int32_t* mclass, const gvo_config* cfgs, int64_t n, PlanShare PS) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  PS.src[c] = -1;
+  const gvo_config cfg = cfgs[c];
+  if (cfg.work_per_thread < 0 || cfg.work_per_thread >= (int64_t(1) << 31)) return;
+  const int tpl = cfg.template_id;
+  const int tcls = T.tclass ? T.tclass[tpl] : -1;
+  uint64_t key[kPlanKey];
+  key[0] = tcls >= 0 ? (uint64_t)tcls : ((uint64_t)1 << 40) | (uint64_t)tpl;
+  key[1] = (uint64_t)(uint32_t)cfg.block[0] | ((uint64_t)(uint32_t)cfg.block[1] << 21) |
+           ((uint64_t)(uint32_t)cfg.block[2] << 42);
+  key[2] = (uint64_t)cfg.grid[0];
+  key[3] = (uint64_t)cfg.grid[1];
+  key[4] = (uint64_t)cfg.grid[2];
+  key[5] = (uint64_t)cfg.work_per_thread | ((uint64_t)(uint32_t)mclass[cfg.machine_id] << 32);
+  uint64_t h = 0x13198a2e03707344ull;
+#pragma unroll
+  for (int k = 0; k < kPlanKey; ++k) h = pmix(h, key[k]);
+  const uint64_t tag = h | 1ull;
+  int64_t slot = (int64_t)(h >> 9) & PS.mask;
+  for (int p = 0; p < kPlanProbe; ++p, slot = (slot + 1) & PS.mask) {
+    PlanEntry& e = PS.table[slot];
+    const unsigned long long old = atomicCAS(&e.tag, 0ull, (unsigned long long)tag);
+    if (old == 0ull) {  // claimed: leader of its key
+      const unsigned long long s = atomicAdd(PS.n_used, 1ull);
+      const int cs = s < (unsigned long long)PS.cap ? (int)s : -1;
+      for (int k = 0; k < kPlanKey; ++k) e.key[k] = key[k];
+      e.slot = cs;
+      __threadfence();
+      atomicExch(&e.ready, 1);
+      if (cs >= 0) PS.src[c] = -2 - cs;
+      return;
+    }
+    if (old != tag) continue;
+    while (atomicAdd(&e.ready, 0) == 0) __nanosleep(32);
+    __threadfence();
+    bool same = true;
+#pragma unroll
+    for (int k = 0; k < kPlanKey; ++k) same &= *reinterpret_cast<volatile uint64_t*>(&e.key[k]) == key[k];
+    if (same) {
+      const int cs = *reinterpret_cast<volatile int*>(&e.slot);
+      PS.src[c] = cs >= 0 ? cs : -1;
+      return;
+    }
+  }
+}
+
+// The plan of one configuration, all threads of the CTA (256).  A leader
+// (src <= -2) also fills its cache slot.
+__device__ void setup_one(const TplView& T, const gvo_machine* machines, const gvo_config* cfgs, int64_t c,
+                          const gvo_sampling& smp, int64_t* coefs, Geo* geos, int64_t* ctabs, int64_t* cache_slot) {
   extern __shared__ int16_t sh16[];
   __shared__ Geo G;
   __shared__ unsigned long long first_fail;
-  const int64_t c = blockIdx.x;
-  if (c >= n) return;
+  __shared__ unsigned long long s_mag;  // largest |coefficient| / |guard bound| of any node
+  if (threadIdx.x == 0) s_mag = 0;
+  __syncthreads();
   const gvo_config cfg = cfgs[c];
   const int tpl = cfg.template_id;
   const gvo_machine m = machines[cfg.machine_id];
@@ -229,9 +319,11 @@ __global__ void __launch_bounds__(256) k_setup(TplView T, const gvo_machine* mac
   for (int a = threadIdx.x; a < A; a += blockDim.x) {
     const int ga = abase + a;
     AffineForm f;
-    int flag = affine_extract(T.code + T.code_off[ga], T.code_len[ga], bd, fbase, &f);
+    uint64_t mag = 0;
+    int flag = affine_extract(T.code + T.code_off[ga], T.code_len[ga], bd, fbase, &f, cache_slot ? &mag : nullptr);
     for (int k = 0; k < 7; ++k) crow[a * 8 + k] = flag == kAffine ? f.c[k] : 0;
     crow[a * 8 + 7] = flag;
+    if (cache_slot && mag) atomicMax(&s_mag, (unsigned long long)mag);
   }
   __syncthreads();
   build_classes_cta(T, tpl, crow, CTab{ctabs + c * ctab_stride(T.max_acc), T.max_acc}, sh16, sh16 + ((T.max_acc + 1) & ~1));
@@ -354,7 +446,11 @@ __global__ void __launch_bounds__(256) k_setup(TplView T, const gvo_machine* mac
       run_bid_bounds(rs, rc, gd, clo + 3, chi + 3);
       const int ga = abase + a;
       int64_t lo, hi;
-      if (bounds_check(T.code + T.code_off[ga], T.code_len[ga], clo, chi, bd, fbase, &lo, &hi) >= 0) {
+      uint64_t mag = 0;
+      const int bad = bounds_check(T.code + T.code_off[ga], T.code_len[ga], clo, chi, bd, fbase, &lo, &hi,
+                                   cache_slot ? &mag : nullptr);
+      if (cache_slot && mag) atomicMax(&s_mag, (unsigned long long)mag);
+      if (bad >= 0) {
         // order inside a group: phase 0 field-major (volumes.py:164-171);
         // phase 1 field, loads before stores (footprint.py:541-545);
         // phase 2 kernel order (volumes.py:126)
@@ -424,14 +520,105 @@ __global__ void __launch_bounds__(256) k_setup(TplView T, const gvo_machine* mac
     uint32_t* dst = reinterpret_cast<uint32_t*>(geos + c);
     for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
   }
+  if (cache_slot) {  // leader: the plan into the call's cache
+    const int64_t A8 = (int64_t)T.max_acc * 8, CS = ctab_stride(T.max_acc);
+    if (threadIdx.x == 0) cache_slot[0] = G.status == GVO_OK && s_mag <= kPlanMag;
+    for (int f = threadIdx.x; f < kMaxFields; f += blockDim.x) cache_slot[1 + f] = f < F ? fbase[f] : 0;
+    const int words = (int)(sizeof(Geo) / 4);
+    uint32_t* gdst = reinterpret_cast<uint32_t*>(cache_slot + plan_geo_off());
+    const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(&G);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) gdst[i] = gsrc[i];
+    for (int64_t i = threadIdx.x; i < (int64_t)A * 8; i += blockDim.x) cache_slot[plan_coef_off() + i] = crow[i];
+    const int64_t* ct = ctabs + c * CS;
+    for (int64_t i = threadIdx.x; i < CS; i += blockDim.x) cache_slot[plan_ctab_off(T.max_acc) + i] = ct[i];
+    (void)A8;
+  }
+}
+
+// One CTA per configuration: leaders and unshared configurations.
+__global__ void __launch_bounds__(256) k_setup(TplView T, const gvo_machine* machines, const gvo_config* cfgs,
+                                               int64_t n, gvo_sampling smp, int64_t* coefs, Geo* geos,
+                                               int64_t* ctabs, PlanShare PS) {
+  const int64_t c = blockIdx.x;
+  if (c >= n) return;
+  const int64_t ps = PS.src ? PS.src[c] : -1;
+  if (ps >= 0) return;  // a follower: k_plan_follow
+  setup_one(T, machines, cfgs, c, smp, coefs, geos, ctabs,
+            ps <= -2 ? PS.cache + (-2 - ps) * plan_slot_words(T.max_acc) : nullptr);
+}
+
+// One CTA per configuration: followers take their leader's plan with the
+// field-base shifts, or compute it when the leader's plan is not shareable.
+__global__ void __launch_bounds__(256) k_plan_follow(TplView T, const gvo_machine* machines, const gvo_config* cfgs,
+                                                     int64_t n, gvo_sampling smp, int64_t* coefs, Geo* geos,
+                                                     int64_t* ctabs, PlanShare PS) {
+  const int64_t c = blockIdx.x;
+  if (c >= n) return;
+  const int64_t ps = PS.src[c];
+  if (ps < 0) return;
+  const int64_t* slot = PS.cache + ps * plan_slot_words(T.max_acc);
+  const gvo_config cfg = cfgs[c];
+  const int tpl = cfg.template_id;
+  const int F = T.n_fields[tpl], A = T.n_acc[tpl], abase = T.acc_base[tpl];
+  const int64_t* fbase = T.field_base + T.field_base_off[tpl];
+  __shared__ int64_t dlt[kMaxFields];
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    bool ok = slot[0] != 0;
+    for (int f = 0; f < F && ok; ++f) {
+      const __int128 d = (__int128)fbase[f] - slot[1 + f];
+      ok = d >= -kPlanShift && d <= kPlanShift;
+      dlt[f] = ok ? (int64_t)d : 0;
+    }
+    s_ok = ok;
+  }
+  __syncthreads();
+  if (!s_ok) {
+    setup_one(T, machines, cfgs, c, smp, coefs, geos, ctabs, nullptr);
+    return;
+  }
+  const int words = (int)(sizeof(Geo) / 4);
+  const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(slot + plan_geo_off());
+  uint32_t* gdst = reinterpret_cast<uint32_t*>(geos + c);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) gdst[i] = gsrc[i];
+  // coefficients: the constant of an affine access moves with its field's base
+  const int64_t* csrc = slot + plan_coef_off();
+  int64_t* crow = coefs + c * (int64_t)T.max_acc * 8;
+  for (int i = threadIdx.x; i < A * 8; i += blockDim.x) {
+    const int a = i >> 3, k = i & 7;
+    int64_t v = csrc[i];
+    if (k == 0 && csrc[a * 8 + 7] == kAffine) v += dlt[T.acc_field[abase + a]];
+    crow[i] = v;
+  }
+  // class table: same classes, each class's sorted constants shifted by its field's delta
+  const int64_t CS = ctab_stride(T.max_acc);
+  const int64_t* tsrc = slot + plan_ctab_off(T.max_acc);
+  int64_t* tdst = ctabs + c * CS;
+  const CTab sct{const_cast<int64_t*>(tsrc), T.max_acc}, dct{tdst, T.max_acc};
+  const int64_t n_head = dct.pts() - tdst;  // slot_first, start, cnt, rep
+  for (int64_t i = threadIdx.x; i < n_head; i += blockDim.x) tdst[i] = tsrc[i];
+  const int ncls = (int)sct.slot_first()[2 * kMaxFields];
+  for (int cl = threadIdx.x; cl < ncls; cl += blockDim.x) {
+    const int64_t d = dlt[T.acc_field[abase + (int)sct.rep()[cl]]];
+    const int64_t s0 = sct.start()[cl], m = sct.cnt()[cl];
+    for (int64_t q = 0; q < m; ++q) dct.pts()[s0 + q] = sct.pts()[s0 + q] + d;
+  }
 }
 
 void launch_setup(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs,
                   int64_t n, const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos, int64_t* d_ctabs,
-                  cudaStream_t st) {
-  if (n > 0)
-    k_setup<<<(unsigned)n, 256, setup_smem(T.max_acc), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs,
-                                                                       d_geos, d_ctabs);
+                  cudaStream_t st, const int32_t* d_mclass, const PlanShare* share) {
+  if (n <= 0) return;
+  PlanShare PS{};
+  if (share && share->table && d_mclass) {
+    PS = *share;
+    k_plan_key<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(T, d_mclass, d_cfgs, n, PS);
+  }
+  k_setup<<<(unsigned)n, 256, setup_smem(T.max_acc), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs, d_geos, d_ctabs,
+                                                           PS);
+  if (PS.src)
+    k_plan_follow<<<(unsigned)n, 256, setup_smem(T.max_acc), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs, d_geos,
+                                                                   d_ctabs, PS);
 }
 
 __global__ void k_classes_only(TplView T, const gvo_config* cfgs, int64_t n, const int64_t* coefs,

@@ -76,3 +76,33 @@ def test_sharing_respects_machine_integer_parameters():
     for k in ("counts", "l1_access"):
         assert np.array_equal(on[k], off[k]), k
     assert np.array_equal(on["records"].view(np.int64), off["records"].view(np.int64))
+
+
+def test_plan_sharing_with_failing_leaders():
+    """Plan sharing (k_setup.cu): configurations equal up to field-base
+    translation and machine capacities take their leader's plan; a leader
+    whose plan is not shareable (here: a FootprintError, 1024-thread blocks
+    on a machine limited to 512 threads per block) leaves every follower to
+    compute its own — statuses and records equal the unshared run's."""
+    import dataclasses
+
+    from paper_2107_01143_b200.gvo.machine import b200_preset
+
+    m = b200_preset()
+    ms = [m, dataclasses.replace(m, name="l2-quarter", l2_capacity_bytes=m.l2_capacity_bytes // 4),
+          dataclasses.replace(m, name="tpb-512", max_threads_per_block=512)]
+    sp = W.space_c3(m, radii=(1,), components=(2,), alignments=(0, 8, 16, 136), machines=ms, machines_idx=(0, 1, 2))
+    ctx = _native.context()
+    cfgs = sp.config_array(ctx)
+    try:
+        off, _, _ = _run(ctx, cfgs, False)
+        on, _, follow = _run(ctx, cfgs, True)
+    finally:
+        _native.lib().gvo_set_dedup(ctx.h, 1)
+    st = on["counts"][:, _native.C_STATUS]
+    assert (st != 0).sum() > 0 and (st == 0).sum() > 0
+    assert follow > 0
+    for k in ("counts", "l1_access"):
+        assert np.array_equal(on[k], off[k]), k
+    for k in ("stats", "records"):
+        assert np.array_equal(on[k].view(np.int64), off[k].view(np.int64)), k
