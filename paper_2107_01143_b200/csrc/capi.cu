@@ -94,6 +94,10 @@ struct gvo_ctx {
   DBuf<PlanEntry> plan_table;
   DBuf<int64_t> plan_cache, plan_src;
   DBuf<unsigned long long> plan_used;
+  // work lists of the set kernel (k_dedup.cu k_worklist), per batch
+  bool worklist = true;
+  DBuf<int32_t> wl_list;
+  DBuf<unsigned long long> wl_cnt;
   DBuf<DedupEntry> dd_table;
   int64_t dd_mask = 0;
   DBuf<int64_t> dd_lead;
@@ -294,6 +298,7 @@ int gvo_open(int device, gvo_ctx** out) {
   if (const char* e = getenv("GVO_BIG_BATCH")) { ctx->big_batch = atoll(e); ctx->big_forced = true; }
   if (const char* e = getenv("GVO_DEDUP")) ctx->dedup = atoi(e) != 0;
   if (const char* e = getenv("GVO_PLAN_SHARE")) ctx->plan_share = atoi(e) != 0;
+  if (const char* e = getenv("GVO_WORKLIST")) ctx->worklist = atoi(e) != 0;
   ctx->n_ctas = kMaxSetsCtasPerSm * ctx->n_sm;
   *out = ctx;
   return GVO_OK;
@@ -315,6 +320,8 @@ void gvo_close(gvo_ctx* ctx) {
   ctx->plan_cache.release();
   ctx->plan_src.release();
   ctx->plan_used.release();
+  ctx->wl_list.release();
+  ctx->wl_cnt.release();
   ctx->dd_lead.release();
   ctx->t_code.release();
   ctx->d_machines.release();
@@ -642,6 +649,13 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     L.pat_off = ctx->pat_off;
     L.wave_field_major = ctx->wave_fm;
     L.lead = lead;
+    if (ctx->worklist && S > 0) {
+      if (!ctx->wl_list.ensure((size_t)dedup_units(nb, F, S)) || !ctx->wl_cnt.ensure(3))
+        return set_err(ctx, GVO_ERR_CUDA, "work list alloc failed%s");
+      launch_worklists(ctx->view, cf, ctx->geos.p, nb, F, S, lead, ctx->wave_fm ? 1 : 0, ctx->wl_list.p,
+                       ctx->wl_cnt.p, &L.wl_wave, &L.wl_blk, &L.wl_warp, st);
+      L.wl_cnt = ctx->wl_cnt.p;
+    }
     if (fuse) {
       L.warp = WA;
       L.n_warp_items = WA.n_items;

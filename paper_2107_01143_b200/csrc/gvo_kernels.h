@@ -80,6 +80,11 @@ struct SetsLaunch {
   int32_t wave_field_major = 1;
   int32_t epoch = 1;  // launch number, unique across both residencies (queue readiness tag)
   const int64_t* lead = nullptr;  // k_dedup: >= 0 = unit copied from another config's (skip)
+  // work lists (k_dedup.cu k_worklist), mode 0; null = every item
+  const int32_t* wl_wave = nullptr;
+  const int32_t* wl_blk = nullptr;
+  const int32_t* wl_warp = nullptr;
+  const unsigned long long* wl_cnt = nullptr;
 };
 namespace sets1 {
 int64_t sets_ebuf_bytes();
@@ -104,6 +109,12 @@ int64_t dedup_units(int64_t n, int F, int S);
 void launch_dedup(const TplView& T, const gvo_machine* d_machines, const int32_t* d_mclass, const gvo_config* d_cfgs,
                   const Geo* d_geos, int64_t n, int F, int S, int64_t b0, DedupEntry* table, int64_t mask,
                   int64_t* d_lead, unsigned long long* d_stats, cudaStream_t st);
+// work lists of the set kernel for one batch: wave units (in the kernel's
+// wave order), block units and warp items that compute; d_list holds
+// dedup_units(n, F, S) entries, d_cnt three counters
+void launch_worklists(const TplView& T, const gvo_config* d_cfgs, const Geo* d_geos, int64_t n, int F, int S,
+                      const int64_t* d_lead, int wave_field_major, int32_t* d_list, unsigned long long* d_cnt,
+                      const int32_t** wl_wave, const int32_t** wl_blk, const int32_t** wl_warp, cudaStream_t st);
 void launch_dedup_copy(const gvo_config* d_cfgs, const Geo* d_geos, const TplView& T, int64_t* d_counts_all,
                        int64_t counts_stride, int64_t n, int F, int S, int64_t b0, const int64_t* d_lead,
                        int64_t* d_l1_access_all, int32_t l1_stride, cudaStream_t st);

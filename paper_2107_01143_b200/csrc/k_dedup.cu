@@ -235,4 +235,63 @@ void launch_dedup_copy(const gvo_config* d_cfgs, const Geo* d_geos, const TplVie
                                                                 S, b0, d_lead, d_l1_access_all, l1_stride);
 }
 
+// ------------------------------------------------------------------ work lists
+// The set kernel's queue hands out every unit of the batch; after sharing
+// most of them are copies (k_dedup) or empty (fields a template lacks,
+// samples beyond the grid, translate-duplicate samples, failed phases).
+// One thread per unit of a segment (0 wave units in the kernel's wave order,
+// 1 block units, 2 warp items) keeps the units that compute; warp-aggregated
+// appends keep the lists close to item order (heavy wave fields first).
+// The set kernel re-checks every condition, so the lists only need to be a
+// superset of the computing units.
+__global__ void k_worklist(TplView T, const gvo_config* cfgs, const Geo* geos, int64_t n, int F, int S,
+                           const int64_t* lead, int seg, int wave_fm, int32_t* out, unsigned long long* cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = seg == 0 ? n * F : seg == 1 ? n * F * S : n * (S + 1);
+  bool keep = false;
+  if (i < total) {
+    int64_t c, u;
+    int f = 0, j = 0;
+    if (seg == 0) {
+      if (wave_fm) { f = (int)(i / n); c = i % n; }
+      else { c = i / F; f = (int)(i % F); }
+      u = c * F + f;
+    } else if (seg == 1) {
+      c = i / ((int64_t)F * S); f = (int)((i / S) % F); j = (int)(i % S);
+      u = n * F + i;
+    } else {
+      c = i / (S + 1); j = (int)(i % (S + 1));
+      u = n * F * (S + 1) + i;
+    }
+    const Geo& G = geos[c];
+    const int nf = T.n_fields[cfgs[c].template_id];
+    keep = !lead || lead[u] < 0;
+    if (seg == 0) keep = keep && f < nf && phase_ok(G, 1);
+    else if (seg == 1) keep = keep && f < nf && phase_ok(G, 0) && j < G.n_samples && G.dup_of[f][j] < 0;
+    else keep = keep && (j == S ? phase_ok(G, 2) : phase_ok(G, 0) && j < G.n_samples);
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, keep);
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == 0 && bal) base = atomicAdd(&cnt[seg], (unsigned long long)__popc(bal));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (keep) out[base + __popc(bal & ((1u << lane) - 1u))] = (int32_t)i;
+}
+
+void launch_worklists(const TplView& T, const gvo_config* d_cfgs, const Geo* d_geos, int64_t n, int F, int S,
+                      const int64_t* d_lead, int wave_field_major, int32_t* d_list, unsigned long long* d_cnt,
+                      const int32_t** wl_wave, const int32_t** wl_blk, const int32_t** wl_warp, cudaStream_t st) {
+  const int64_t seg_n[3] = {n * F, n * F * S, n * (S + 1)};
+  cudaMemsetAsync(d_cnt, 0, 3 * sizeof(unsigned long long), st);
+  int32_t* out = d_list;
+  const int32_t** dst[3] = {wl_wave, wl_blk, wl_warp};
+  for (int seg = 0; seg < 3; ++seg) {
+    *dst[seg] = out;
+    if (seg_n[seg] > 0)
+      k_worklist<<<(unsigned)((seg_n[seg] + 255) / 256), 256, 0, st>>>(T, d_cfgs, d_geos, n, F, S, d_lead, seg,
+                                                                        wave_field_major, out, d_cnt);
+    out += seg_n[seg];
+  }
+}
+
 }  // namespace gvo

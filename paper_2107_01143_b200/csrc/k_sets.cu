@@ -1887,6 +1887,14 @@ struct SetsArgs {
   int32_t wave_field_major; // wave units ordered field-major (heavy fields first)
   int32_t epoch;            // launch number; queue slots are ready when ready == epoch
   const int64_t* lead;      // mode 0, k_dedup.cu: >= 0 = unit copied from an identical one (skip); may be null
+  // mode 0 work lists (k_dedup.cu k_worklist): the wave units, block units
+  // and warp items that compute, in item order; counts on the device.  The
+  // work queue then hands out list entries only (copied and empty units are
+  // never fetched, bundles of block units are dense).  May be null.
+  const int32_t* wl_wave;
+  const int32_t* wl_blk;
+  const int32_t* wl_warp;
+  const unsigned long long* wl_cnt;
 };
 
 // ------------------------------------------------------------------ micro tier
@@ -2174,6 +2182,14 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
   const int64_t n_bund = micro_on ? (n_blk_u + kNW - 1) / kNW : 0;
   const int64_t n_set_main = micro_on ? n_wave_u + n_bund : P.n_items;
   const int64_t n_main = n_set_main + P.n_warp_items;
+  // work lists: the queue runs over list entries (virtual items), mapped back
+  // to the item space at fetch
+  const bool use_wl = micro_on && P.wl_cnt != nullptr;
+  const int64_t n_wave_l = use_wl ? (int64_t)P.wl_cnt[0] : n_wave_u;
+  const int64_t n_blk_l = use_wl ? (int64_t)P.wl_cnt[1] : n_blk_u;
+  const int64_t n_bund_l = use_wl ? (n_blk_l + kNW - 1) / kNW : n_bund;
+  const int64_t n_set_main_l = use_wl ? n_wave_l + n_bund_l : n_set_main;
+  const int64_t n_main_l = use_wl ? n_set_main_l + (P.n_warp_items > 0 ? (int64_t)P.wl_cnt[2] : 0) : n_main;
   const int64_t kBlkBase = int64_t(1) << 40;
 
 #if defined(GVO_DEBUG_SYNC) && GVO_DEBUG_SYNC
@@ -2233,12 +2249,17 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           // items never do (the counter only grows, so a peek past the wave
           // units stays past them)
           const int64_t peek = (int64_t)vload(P.work);
-          const bool may_split = P.mode != 0 || peek < n_wave_u;
+          const bool may_split = P.mode != 0 || peek < n_wave_l;
           if (!may_split || slot_free()) {
             const unsigned long long m = atomicAdd(P.work, 1ull);
-            if ((int64_t)m < n_main) {
+            if ((int64_t)m < n_main_l) {
               kind = 0;
               it = (int64_t)m;
+              if (use_wl) {  // list entry -> item (bundles stay virtual: their warps read the block list)
+                if (it < n_wave_l) it = P.wl_wave[it];
+                else if (it < n_set_main_l) it = n_wave_u + (it - n_wave_l);
+                else it = n_set_main + P.wl_warp[it - n_set_main_l];
+              }
               if (SS) atomicAdd(&SS->pending, 1ull);
               break;
             }
@@ -2294,7 +2315,8 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
     if (!in_range && micro_on && item >= n_wave_u && item < n_set_main) {
       // bundle of kNW block units, one per warp
       const int w = threadIdx.x >> 5;
-      const int64_t bidx = (item - n_wave_u) * kNW + w;
+      int64_t bidx = (item - n_wave_u) * kNW + w;
+      if (use_wl) bidx = bidx < n_blk_l ? P.wl_blk[bidx] : n_blk_u;
       if (bidx < n_blk_u) {
         const bool ok = micro_unit(P, bidx, micro_region + w * kMicroBytes, cpts + w * kClassPts,
                                    runs + w * kMicroRunCap);
@@ -3206,6 +3228,10 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st) {
   P.seg_off = L.seg_off;
   P.pat_off = L.pat_off;
   P.lead = L.lead;
+  P.wl_wave = L.wl_wave;
+  P.wl_blk = L.wl_blk;
+  P.wl_warp = L.wl_warp;
+  P.wl_cnt = L.wl_cnt;
   P.wave_field_major = L.wave_field_major;
   P.epoch = L.epoch;  // never 0 (the zeroed initial state), unique per launch
   if (P.n_items + P.n_warp_items <= 0) return;
