@@ -84,7 +84,20 @@ __shared__ int gvo_dbg_wexit[3];
 #define GVO_DBG_WEXIT(k) do { } while (0)
 #endif
 
-static __device__ __noinline__ void warp_item(const WarpArgs& W, int64_t item, unsigned long long* sh) {
+// inlined into its callers: as an out-of-line call (early returns before
+// its barriers) compute-sanitizer synccheck reports a divergent barrier at
+// the caller's next __syncthreads although every warp takes the same exit
+// (checked at run time with -DGVO_DEBUG_SYNC); inlined, synccheck is clean.
+// GVO_WARP_ITEM_INLINE=0 restores the call (A/B).
+#ifndef GVO_WARP_ITEM_INLINE
+#define GVO_WARP_ITEM_INLINE 1
+#endif
+#if GVO_WARP_ITEM_INLINE
+#define GVO_WI_ATTR __forceinline__
+#else
+#define GVO_WI_ATTR __noinline__
+#endif
+static __device__ GVO_WI_ATTR void warp_item(const WarpArgs& W, int64_t item, unsigned long long* sh) {
   const TplView& T = W.T;
   const gvo_machine* machines = W.machines;
   const gvo_config* cfgs = W.cfgs;

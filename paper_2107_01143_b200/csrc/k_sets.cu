@@ -2298,7 +2298,6 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
     if (!in_range && item >= n_set_main && item < kBlkBase) {
 #if defined(GVO_DEBUG_SYNC) && GVO_DEBUG_SYNC
       if (threadIdx.x < 3) gvo_dbg_wexit[threadIdx.x] = 0;
-      __syncthreads();
 #endif
       warp_item(P.warp, item - n_set_main, reinterpret_cast<unsigned long long*>(ebuf));
       __syncthreads();
@@ -2785,10 +2784,10 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         bm_r_ok = bm_r_ok && U.sub_r[q] >= 1 && U.sub_r[q] <= 32 && (32 % U.sub_r[q]) == 0;
       const int64_t bm_words = sm_elems * 4;  // ebuf holds 2*sm_elems 8-byte elements
       const bool has_pat = *reinterpret_cast<volatile const int32_t*>(&hdr->has_pattern) != 0;
-      // reset here and at the end of every pass that continues (by thread
-      // 0, before the pass's last barrier): the loop-exit read of s_split
-      // is a vector load that also covers s_nonmono, so a reset at the top
-      // of the loop would race with it
+      // reset here and by thread 0 when a pass continues (before the pass's
+      // last barrier): the loop-exit read of s_split is a vector load that
+      // also covers s_nonmono, so a reset at the top of the loop would race
+      // with it
       if (threadIdx.x == 0) { s_nonmono = 0; s_rtags = 0u; }
       for (;;) {
         // count in-range elements per run (monotone runs: closed form)
@@ -2922,6 +2921,8 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
               }
             }
             s_split = 1;
+            s_nonmono = 0;  // the next pass's
+            s_rtags = 0u;
             cur_range.a = a;
             cur_range.b = a + width;
           }
@@ -2929,7 +2930,6 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           cur_range.a = a;
           cur_range.b = b;
         }
-        if (threadIdx.x == 0 && s_split) { s_nonmono = 0; s_rtags = 0u; }  // the next pass's
         __syncthreads();
         b = cur_range.b;
         if (!s_split) break;
