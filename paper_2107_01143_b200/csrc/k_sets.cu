@@ -1630,6 +1630,30 @@ __device__ __noinline__ void bm_pattern_warp(uint32_t* bmt, const Run* rrp, int6
   }
 }
 
+// popcounts of the atoms of NT bitmap planes over words [0, wp): acc[p] =
+// bits set in exactly the planes of p (p = 1 .. 2^NT - 1), this thread's words
+#ifndef GVO_BM_ATOMS
+#define GVO_BM_ATOMS 1  // 0: the per-measure OR-select pass only (A/B)
+#endif
+constexpr int kAtomTags = 4;
+template <int NT>
+__device__ __forceinline__ void atom_counts(const uint32_t* bm, int64_t wp, int32_t (&acc)[1 << kAtomTags]) {
+#pragma unroll
+  for (int p = 0; p < (1 << kAtomTags); ++p) acc[p] = 0;
+  for (int64_t i = threadIdx.x; i < wp; i += kNT) {
+    uint32_t tw[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) tw[t] = bm[(int64_t)t * wp + i];
+#pragma unroll
+    for (int p = 1; p < (1 << NT); ++p) {
+      uint32_t v = ~0u;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) v &= ((p >> t) & 1) ? tw[t] : ~tw[t];
+      acc[p] += __popc(v);
+    }
+  }
+}
+
 __device__ __noinline__ void bitmap_range(uint32_t* bm, const Run* druns, const int64_t* rcnt, const int64_t* rka, int nr,
                              int64_t N, int64_t a, int64_t b, int64_t kbase, int n_tags, const Granule& Gr,
                              const TplView& T, int abase, const int64_t* fbase, const int32_t bd[3],
@@ -1785,6 +1809,47 @@ __device__ __noinline__ void bitmap_range(uint32_t* bm, const Run* druns, const 
   }
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // granule-resolution measures over <= 4 planes (wave-unit pieces): per word
+  // the popcounts of the 2^T - 1 atoms (bits in exactly the planes of p), and
+  // |union of the planes in S| = sum of the atoms p that meet S — T-1 ANDs per
+  // atom instead of one OR-select per plane and measure
+  bool all_r1 = GVO_BM_ATOMS != 0;
+  for (int q = 0; q < U.n_sub; ++q) all_r1 &= U.sub_r[q] == 1;
+  if (all_r1 && n_tags <= kAtomTags) {
+    if (threadIdx.x < U.n_sub) {
+      uint32_t cmq = 0;
+      for (uint32_t m = U.sub_mask[threadIdx.x] & tag_mask; m; m &= m - 1)
+        cmq |= 1u << __popc(tag_mask & ((1u << (__ffs(m) - 1)) - 1u));
+      U.sub_cm[threadIdx.x] = cmq;
+    }
+    int32_t acc[1 << kAtomTags];
+    switch (n_tags) {
+      case 1: atom_counts<1>(bm, wp, acc); break;
+      case 2: atom_counts<2>(bm, wp, acc); break;
+      case 3: atom_counts<3>(bm, wp, acc); break;
+      default: atom_counts<4>(bm, wp, acc); break;
+    }
+    const int np = 1 << n_tags;
+#pragma unroll
+    for (int p = 1; p < (1 << kAtomTags); ++p) {
+      if (p < np) {
+        int32_t v = acc[p];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) wmax[p * kNW + w] = v;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < U.n_sub) {
+      const uint32_t cm = U.sub_cm[threadIdx.x];
+      int64_t t = 0;
+      for (int p = 1; p < np; ++p)
+        if (p & cm)
+          for (int k = 0; k < kNW; ++k) t += wmax[p * kNW + k];
+      U.sub_val[threadIdx.x] = t;
+    }
+    __syncthreads();
+    return;
+  }
   constexpr int kPcSub = 16, kPcTags = 8;
   if (U.n_sub <= kPcSub && n_tags <= kPcTags) {
     // every requested measure in one pass over the words

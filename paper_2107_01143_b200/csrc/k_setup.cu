@@ -529,8 +529,17 @@ __device__ void setup_one(const TplView& T, const gvo_machine* machines, const g
     const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(&G);
     for (int i = threadIdx.x; i < words; i += blockDim.x) gdst[i] = gsrc[i];
     for (int64_t i = threadIdx.x; i < (int64_t)A * 8; i += blockDim.x) cache_slot[plan_coef_off() + i] = crow[i];
-    const int64_t* ct = ctabs + c * CS;
-    for (int64_t i = threadIdx.x; i < CS; i += blockDim.x) cache_slot[plan_ctab_off(T.max_acc) + i] = ct[i];
+    // the class table's defined words: slot heads, per-class start/cnt/rep, the points
+    const CTab src{ctabs + c * CS, T.max_acc}, dst{cache_slot + plan_ctab_off(T.max_acc), T.max_acc};
+    const int ncls = (int)src.slot_first()[2 * kMaxFields];
+    for (int i = threadIdx.x; i <= 2 * kMaxFields; i += blockDim.x) dst.slot_first()[i] = src.slot_first()[i];
+    for (int i = threadIdx.x; i < ncls; i += blockDim.x) {
+      dst.start()[i] = src.start()[i];
+      dst.cnt()[i] = src.cnt()[i];
+      dst.rep()[i] = src.rep()[i];
+    }
+    const int64_t npts = ncls ? src.start()[ncls - 1] + src.cnt()[ncls - 1] : 0;
+    for (int64_t i = threadIdx.x; i < npts; i += blockDim.x) dst.pts()[i] = src.pts()[i];
     (void)A8;
   }
 }
@@ -595,9 +604,13 @@ __global__ void __launch_bounds__(256) k_plan_follow(TplView T, const gvo_machin
   const int64_t* tsrc = slot + plan_ctab_off(T.max_acc);
   int64_t* tdst = ctabs + c * CS;
   const CTab sct{const_cast<int64_t*>(tsrc), T.max_acc}, dct{tdst, T.max_acc};
-  const int64_t n_head = dct.pts() - tdst;  // slot_first, start, cnt, rep
-  for (int64_t i = threadIdx.x; i < n_head; i += blockDim.x) tdst[i] = tsrc[i];
   const int ncls = (int)sct.slot_first()[2 * kMaxFields];
+  for (int i = threadIdx.x; i <= 2 * kMaxFields; i += blockDim.x) dct.slot_first()[i] = sct.slot_first()[i];
+  for (int i = threadIdx.x; i < ncls; i += blockDim.x) {
+    dct.start()[i] = sct.start()[i];
+    dct.cnt()[i] = sct.cnt()[i];
+    dct.rep()[i] = sct.rep()[i];
+  }
   for (int cl = threadIdx.x; cl < ncls; cl += blockDim.x) {
     const int64_t d = dlt[T.acc_field[abase + (int)sct.rep()[cl]]];
     const int64_t s0 = sct.start()[cl], m = sct.cnt()[cl];
