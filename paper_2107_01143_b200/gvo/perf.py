@@ -99,6 +99,14 @@ class SweepRow:
 _FOLD_FACTORS = {"none": (1, 1, 1), "2y": (1, 2, 1), "2z": (1, 1, 2)}
 
 
+# (family, template key) -> (template descriptor, context, template id):
+# generator families build the same descriptor for every sweep, so repeated
+# sweeps skip rebuilding and re-hashing the access trees (descriptors are
+# immutable; file families are not cached: their spec does not enter the
+# family's hash)
+_TPL_CACHE: dict = {}
+
+
 class SweepPlan:
     """A validated sweep in columnar form: the kept configurations (input
     order), one device template per distinct access structure and the
@@ -133,8 +141,9 @@ class SweepPlan:
             except (TypeError, ValueError):
                 ok_shape = False
             if ok_shape:
-                ff = np.array([_FOLD_FACTORS.get(c.folding, (0, 0, 0)) if isinstance(c.folding, str) else (0, 0, 0)
-                               for c in configs], dtype=np.int64)
+                folds = [c.folding for c in configs]
+                ff = np.array([_FOLD_FACTORS.get(f, (0, 0, 0)) if isinstance(f, str) else (0, 0, 0)
+                               for f in folds], dtype=np.int64)
                 g = np.array([int(v) for v in family.grid], dtype=np.int64)
                 eff = b * ff
                 ok = (ff > 0).all(axis=1) & (b >= 1).all(axis=1) & (g >= 1).all()
@@ -150,8 +159,14 @@ class SweepPlan:
                 grid[ok] = g[None, :] // np.where(eff[ok] > 0, eff[ok], 1)
                 wpt[ok] = ff[ok].prod(axis=1)
                 flops[ok] = fl
-                for i in np.flatnonzero(ok):
-                    tkey[i] = family.template_key(configs[i])
+                # stencil / lbm template keys depend on the folding only
+                kf: dict = {}
+                for i in np.flatnonzero(ok).tolist():
+                    f = folds[i]
+                    k = kf.get(f)
+                    if k is None:
+                        k = kf[f] = family.template_key(configs[i])
+                    tkey[i] = k
         self.build_error = None  # (index, exception) of the first invalid config (skip_invalid=False)
         keep = np.ones(n, dtype=bool)
         for i in np.flatnonzero(~fast):
@@ -174,12 +189,22 @@ class SweepPlan:
         self.templates: list = []
         tix: dict = {}
         self.tpl = np.zeros(len(idx), dtype=np.int32)
+        cacheable = family.kind in ("stencil", "lbm")
         for j, i in enumerate(idx):
             t = tix.get(tkey[i])
             if t is None:
                 t = tix[tkey[i]] = len(self.templates)
-                k = family.build(configs[i])
-                self.templates.append((k, ctx.template_id(k.fields, k.accesses)))
+                hit = _TPL_CACHE.get((family, tkey[i])) if cacheable else None
+                if hit is not None and hit[1] is ctx:
+                    self.templates.append((hit[0], hit[2]))
+                else:
+                    k = family.build(configs[i])
+                    tid = ctx.template_id(k.fields, k.accesses)
+                    self.templates.append((k, tid))
+                    if cacheable:
+                        if len(_TPL_CACHE) >= 4096:
+                            _TPL_CACHE.clear()
+                        _TPL_CACHE[(family, tkey[i])] = (k, ctx, tid)
             self.tpl[j] = t
         self.fold_rank = np.array([_engine.FOLD_RANK[c.folding] for c in self.configs], dtype=np.int32)
 
