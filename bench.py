@@ -70,12 +70,17 @@ WORKLOADS = {
 
 def build_shard(workload: str, rank: int, world: int):
     """(whole space, this rank's global indices, padded shard length m).
-    The space is dealt by estimated cost (strong scaling)."""
+    The space is dealt in sharing groups (configurations whose set problems
+    are exact translates stay on one rank) by estimated cost, longest first
+    to the least-loaded rank (strong scaling)."""
     from paper_2107_01143_b200 import shard, workloads as W
 
     sp = W.space(workload, b200_machine())
-    idx = shard.shard_indices(shard.config_cost(sp.block, sp.n_accesses()), world, rank)
-    return sp, idx, shard.pad_to(len(sp), world)
+    if world == 1:
+        return sp, np.arange(len(sp)), len(sp)
+    cost = shard.config_cost(sp.block, sp.n_accesses()) * sp.kind_weight()
+    shards = shard.group_shards(cost, sp.sharing_groups(), world)
+    return sp, shards[rank], max(len(x) for x in shards)
 
 
 class ClockSampler:
@@ -370,7 +375,7 @@ def run_device(args, rank, world):
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "int64", "data": "synthetic (deterministic config-space enumeration)",
         "config": {"workload": WORKLOADS[args.workload], "configs_total": N,
-                   "configs_per_rank_max": m, "parallelism": f"dp{world} (cost-dealt config shards, "
+                   "configs_per_rank_max": m, "parallelism": f"dp{world} (cost-dealt sharing-group shards, "
                    f"{'NCCL' if nccl or world == 1 else 'gloo'} all-gather + device rank)",
                    "l2": "flushed between timed steps (256 MiB write)", "batch": int(os.environ.get("GVO_BATCH", 16384))},
         "e2e": e2e,

@@ -28,6 +28,39 @@ def shard_indices(cost: np.ndarray, world: int, rank: int) -> np.ndarray:
     return np.sort(order[rank::world])
 
 
+# Relative device cost of one configuration's computed work per template
+# kind, measured on one B200 (C5 halves evaluated separately, DESIGN.md §5:
+# stencil part 311 ms over its sharing groups' config_cost sum 3.4e8, LBM
+# part 186 ms over 4.8e7): an LBM unit costs ~4.2x a stencil unit of equal
+# config_cost (bitmap-tier key ranges, pattern runs).
+KIND_WEIGHT = {"star": 1.0, "jacobi2d": 1.0, "lbm": 4.2}
+
+
+def group_shards(cost: np.ndarray, group: np.ndarray, world: int) -> list[np.ndarray]:
+    """Every rank's shard when configurations that share work (equal
+    ``group`` id: exact translates of one another's set problems, see
+    csrc/k_dedup.cu) must stay on one rank: the sharing is per rank, so a
+    group split over ranks is computed once per rank.  A group costs its
+    most expensive member (the others copy); groups are dealt longest
+    first to the least-loaded rank (LPT), deterministically.  Returns the
+    sorted global indices of each rank."""
+    import heapq
+
+    cost = np.asarray(cost, dtype=np.float64)
+    gid, inv = np.unique(np.asarray(group), return_inverse=True)
+    gcost = np.zeros(len(gid))
+    np.maximum.at(gcost, inv, cost)
+    order = np.argsort(-gcost, kind="stable")
+    owner = np.empty(len(gid), dtype=np.int64)
+    heap = [(0.0, r) for r in range(world)]
+    for g in order.tolist():
+        load, r = heapq.heappop(heap)
+        owner[g] = r
+        heapq.heappush(heap, (load + float(gcost[g]), r))
+    mine = owner[inv]
+    return [np.flatnonzero(mine == r) for r in range(world)]
+
+
 def pad_to(n: int, world: int) -> int:
     """Shard length every rank pads to (all-gather needs equal sizes)."""
     return -(-n // world)

@@ -298,6 +298,37 @@ class Space:
         per_t = np.array([t.n_accesses() for t in self.templates], dtype=np.int64)
         return per_t[self.tpl]
 
+    def kind_weight(self) -> np.ndarray:
+        """Per-configuration device cost weight of its template kind (shard.KIND_WEIGHT)."""
+        from .shard import KIND_WEIGHT
+
+        per_t = np.array([KIND_WEIGHT.get(t.kind, 1.0) for t in self.templates])
+        return per_t[self.tpl]
+
+    def sharing_groups(self, sector_bytes: int = 32) -> np.ndarray:
+        """Group id per configuration: equal ids share their wave sets on the
+        device (csrc/k_dedup.cu: same accesses up to the field base, base
+        residue modulo the sector, launch and machine integer parameters)."""
+        tkey = {}
+        tcls = np.zeros(len(self.templates), dtype=np.int64)
+        for t, spec in enumerate(self.templates):
+            k = dataclasses.replace(spec, alignment=spec.alignment % sector_bytes)
+            tcls[t] = tkey.setdefault(k, len(tkey))
+        mkey = {}
+        mcls = np.zeros(len(self.machines), dtype=np.int64)
+        for j, m in enumerate(self.machines):
+            k = (m.sm_count, m.l1_line_bytes, m.sector_bytes, m.l1_banks, m.bank_width_bytes,
+                 m.max_threads_per_sm, m.max_blocks_per_sm, m.max_threads_per_block)
+            mcls[j] = mkey.setdefault(k, len(mkey))
+        b = self.block.astype(np.int64)
+        if len(tkey) < (1 << 20) and len(mkey) < (1 << 10) and (b < (1 << 11)).all() and (b >= 0).all():
+            key = ((tcls[self.tpl] << 10 | mcls[self.mach]) << 33) | (b[:, 0] << 22) | (b[:, 1] << 11) | b[:, 2]
+            _, gid = np.unique(key, return_inverse=True)
+        else:
+            key = np.stack([tcls[self.tpl], mcls[self.mach], b[:, 0], b[:, 1], b[:, 2]], axis=1)
+            _, gid = np.unique(key, axis=0, return_inverse=True)
+        return gid.reshape(-1)
+
 
 def pow2_shapes(threads: Sequence[int], x_max=512, y_max=512, z_max=64) -> np.ndarray:
     """Power-of-two (X, Y, Z), X*Y*Z in ``threads`` (reference kernels.py:367-395 order per count)."""

@@ -52,6 +52,39 @@ def test_shard_partition_is_exact_and_balanced():
     assert max(loads) / min(loads) < 1.1
 
 
+def test_group_shards_keep_sharing_groups_whole_and_balance():
+    """Sharing groups (bench.py's strong-scaled C5 sharding) never straddle
+    ranks, every configuration lands on exactly one rank, and the dealt
+    group costs stay balanced."""
+    from paper_2107_01143_b200 import workloads as W
+    from paper_2107_01143_b200.gvo.machine import b200_preset
+
+    m = b200_preset()
+    sp = W.space_c3(m, radii=(2,), components=(2,), alignments=tuple(range(0, 128, 8)), machines=W.l2_variants(m),
+                    machines_idx=(0, 1, 2))
+    g = sp.sharing_groups()
+    cost = shard.config_cost(sp.block, sp.n_accesses()) * sp.kind_weight()
+    for world in (2, 3, 8):
+        parts = shard.group_shards(cost, g, world)
+        allidx = np.concatenate(parts)
+        assert sorted(allidx.tolist()) == list(range(len(sp)))
+        owner = np.empty(len(sp), dtype=np.int64)
+        for r, p_ in enumerate(parts):
+            owner[p_] = r
+        for gid in np.unique(g)[:500]:
+            assert len(np.unique(owner[g == gid])) == 1
+        gc = np.zeros(g.max() + 1)
+        np.maximum.at(gc, g, cost)
+        loads = [gc[np.unique(g[p_])].sum() for p_ in parts]
+        assert max(loads) / min(loads) < 1.05
+    # alignments equal modulo the sector share a group; other residues do not
+    t0 = [i for i, t in enumerate(sp.templates) if t.alignment in (0, 32)]
+    t1 = [i for i, t in enumerate(sp.templates) if t.alignment == 8]
+    a = np.flatnonzero(np.isin(sp.tpl, t0))
+    b = np.flatnonzero(np.isin(sp.tpl, t1))
+    assert len(np.unique(g[a])) < len(a) and not set(g[a]) & set(g[b])
+
+
 def test_gloo_world2_all_gather_reassembles_every_config():
     world, n = 2, 37
     ctx = mp.get_context("spawn")
