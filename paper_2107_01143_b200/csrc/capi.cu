@@ -129,6 +129,8 @@ struct gvo_ctx {
   int64_t big_batch = 1024;
   bool big_forced = false;
   bool all_wide = false;     // every registered template has >= 3 fields
+  bool any_wide = false;     // some registered template has >= 3 fields
+  DBuf<int> wide_flag;       // per batch: 0 = every config's template has >= 3 fields
   int32_t epoch = 0;     // set-kernel launch counter (queue readiness tag)
   DBuf<uint8_t> rank_scratch;
   // host-variant staging
@@ -322,6 +324,7 @@ void gvo_close(gvo_ctx* ctx) {
   ctx->plan_used.release();
   ctx->wl_list.release();
   ctx->wl_cnt.release();
+  ctx->wide_flag.release();
   ctx->dd_lead.release();
   ctx->t_code.release();
   ctx->d_machines.release();
@@ -439,7 +442,11 @@ int gvo_set_templates(gvo_ctx* ctx, const gvo_template* t, int32_t n) {
   ctx->h_nacc = na;
   ctx->h_nfields = nf;
   ctx->all_wide = !nf.empty();
-  for (int32_t f : nf) ctx->all_wide = ctx->all_wide && f >= 3;
+  ctx->any_wide = false;
+  for (int32_t f : nf) {
+    ctx->all_wide = ctx->all_wide && f >= 3;
+    ctx->any_wide = ctx->any_wide || f >= 3;
+  }
   TplView& V = ctx->view;
   V.n_tpl = n;
   V.n_fields = ctx->t_nf.p; V.n_acc = ctx->t_na.p; V.acc_base = ctx->t_ab.p; V.field_base_off = ctx->t_fbo.p;
@@ -613,8 +620,15 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
                d_l1_access ? d_l1_access + b0 * l1_stride * 3 : nullptr, l1_stride, nullptr,
                lead ? lead + nb * F * (S + 1) : nullptr};
     const bool big = nb >= ctx->big_batch && (ctx->big_forced || ctx->all_wide);
+    // mixed registries (e.g. C5: stencil and LBM templates): the residency is
+    // chosen per batch on the device (every config's template has >= 3
+    // fields -> the 1-CTA build), both launches queued, the other one exits
+    const bool pick = !big && !ctx->big_forced && nb >= ctx->big_batch && ctx->any_wide;
     const bool fuse = ctx->fuse_warp &&
-                      (int64_t)warp_item_smem(ctx->max_acc) <= (big ? sets1::sets_ebuf_bytes() : sets2::sets_ebuf_bytes());
+                      (int64_t)warp_item_smem(ctx->max_acc) <=
+                          (big ? sets1::sets_ebuf_bytes()
+                               : pick ? std::min(sets1::sets_ebuf_bytes(), sets2::sets_ebuf_bytes())
+                                      : sets2::sets_ebuf_bytes());
     if (!fuse) {
       tmark_begin(ctx, 1, st, &tb);
       launch_warp(ctx->view, ctx->d_machines.p, cf, ctx->geos.p, ctx->coefs.p, nb * (S + 1), S, m0.sector_bytes,
@@ -672,6 +686,19 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     if (big) {
       L.n_ctas = ctx->n_sm;
       sets1::launch_sets(L, st);
+    } else if (pick) {
+      if (!ctx->wide_flag.ensure(1)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
+      launch_batch_wide(ctx->view, cf, nb, ctx->wide_flag.p, st);
+      SetsLaunch L1 = L;
+      L1.n_ctas = ctx->n_sm;
+      L1.run_if = ctx->wide_flag.p;
+      L1.run_if_val = 0;
+      sets1::launch_sets(L1, st);
+      if (++ctx->epoch == 0) ++ctx->epoch;
+      L.epoch = ctx->epoch;
+      L.run_if = ctx->wide_flag.p;
+      L.run_if_val = 1;
+      sets2::launch_sets(L, st);
     } else {
       sets2::launch_sets(L, st);
     }

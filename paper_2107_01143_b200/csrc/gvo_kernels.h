@@ -85,7 +85,12 @@ struct SetsLaunch {
   const int32_t* wl_blk = nullptr;
   const int32_t* wl_warp = nullptr;
   const unsigned long long* wl_cnt = nullptr;
+  // residency chosen on the device: the launch runs only if *run_if == run_if_val
+  const int* run_if = nullptr;
+  int run_if_val = 0;
 };
+// *d_flag = 0 iff every config of the batch has a template with >= 3 fields (else 1)
+void launch_batch_wide(const TplView& T, const gvo_config* d_cfgs, int64_t n, int* d_flag, cudaStream_t st);
 namespace sets1 {
 int64_t sets_ebuf_bytes();
 void launch_sets(const SetsLaunch& L, cudaStream_t st);

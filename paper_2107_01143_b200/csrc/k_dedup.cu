@@ -25,6 +25,8 @@
 // batches of one call, so a later batch can reuse an earlier batch's counts.
 #include "gvo_kernels.h"
 
+#include <algorithm>
+
 namespace gvo {
 
 namespace {
@@ -292,6 +294,20 @@ void launch_worklists(const TplView& T, const gvo_config* d_cfgs, const Geo* d_g
                                                                         wave_field_major, out, d_cnt);
     out += seg_n[seg];
   }
+}
+
+// *flag = 1 when some config of the batch has a template with < 3 fields
+__global__ void k_batch_wide(TplView T, const gvo_config* cfgs, int64_t n, int* flag) {
+  bool narrow = false;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+    narrow |= T.n_fields[cfgs[c].template_id] < 3;
+  if (__syncthreads_or(narrow) && threadIdx.x == 0) atomicExch(flag, 1);
+}
+
+void launch_batch_wide(const TplView& T, const gvo_config* d_cfgs, int64_t n, int* d_flag, cudaStream_t st) {
+  cudaMemsetAsync(d_flag, 0, sizeof(int), st);
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 1024);
+  k_batch_wide<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(T, d_cfgs, n, d_flag);
 }
 
 }  // namespace gvo

@@ -1960,6 +1960,8 @@ struct SetsArgs {
   const int32_t* wl_blk;
   const int32_t* wl_warp;
   const unsigned long long* wl_cnt;
+  const int* run_if;        // residency picked on the device: run only if *run_if == run_if_val
+  int run_if_val;
 };
 
 // ------------------------------------------------------------------ micro tier
@@ -2202,6 +2204,7 @@ __device__ __forceinline__ unsigned long long vload(const unsigned long long* p)
 }
 
 __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
+  if (P.run_if && *P.run_if != P.run_if_val) return;  // the other residency runs this batch
   extern __shared__ __align__(16) uint8_t smem[];
   UnitSh& U = *reinterpret_cast<UnitSh*>(smem);
   size_t off = (sizeof(UnitSh) + 15) & ~size_t(15);
@@ -3297,6 +3300,8 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st) {
   P.wl_blk = L.wl_blk;
   P.wl_warp = L.wl_warp;
   P.wl_cnt = L.wl_cnt;
+  P.run_if = L.run_if;
+  P.run_if_val = L.run_if_val;
   P.wave_field_major = L.wave_field_major;
   P.epoch = L.epoch;  // never 0 (the zeroed initial state), unique per launch
   if (P.n_items + P.n_warp_items <= 0) return;
