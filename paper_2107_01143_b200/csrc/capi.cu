@@ -94,6 +94,7 @@ struct gvo_ctx {
   DBuf<PlanEntry> plan_table;
   DBuf<int64_t> plan_cache, plan_src;
   DBuf<unsigned long long> plan_used;
+  DBuf<uint8_t> plan_need;
   // work lists of the set kernel (k_dedup.cu k_worklist), per batch
   bool worklist = true;
   DBuf<int32_t> wl_list;
@@ -322,6 +323,7 @@ void gvo_close(gvo_ctx* ctx) {
   ctx->plan_cache.release();
   ctx->plan_src.release();
   ctx->plan_used.release();
+  ctx->plan_need.release();
   ctx->wl_list.release();
   ctx->wl_cnt.release();
   ctx->wide_flag.release();
@@ -585,6 +587,11 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     PS.cap = slots;
     PS.n_used = ctx->plan_used.p;
     PS.src = ctx->plan_src.p;
+    // followers' rows after the work lists, only where a unit computes
+    if (ctx->worklist && ctx->plan_need.ensure((size_t)std::min(n, ctx->batch))) {
+      PS.defer_rows = true;
+      PS.need = ctx->plan_need.p;
+    }
   }
   ctx->dd_units = ctx->dd_follow = 0;
   unsigned long long* dd_stats = nullptr;
@@ -667,8 +674,15 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
       if (!ctx->wl_list.ensure((size_t)dedup_units(nb, F, S)) || !ctx->wl_cnt.ensure(3))
         return set_err(ctx, GVO_ERR_CUDA, "work list alloc failed%s");
       launch_worklists(ctx->view, cf, ctx->geos.p, nb, F, S, lead, ctx->wave_fm ? 1 : 0, ctx->wl_list.p,
-                       ctx->wl_cnt.p, &L.wl_wave, &L.wl_blk, &L.wl_warp, st);
+                       ctx->wl_cnt.p, &L.wl_wave, &L.wl_blk, &L.wl_warp, PS.defer_rows ? ctx->plan_need.p : nullptr,
+                       st);
       L.wl_cnt = ctx->wl_cnt.p;
+    }
+    if (PS.defer_rows) {
+      tmark_begin(ctx, 0, st, &tb);
+      launch_plan_rows(ctx->view, ctx->d_machines.p, cf, nb, *sampling, ctx->coefs.p, ctx->geos.p, ctx->ctabs.p, PS,
+                       st);
+      tmark_end(ctx, 0, st, tb);
     }
     if (fuse) {
       L.warp = WA;

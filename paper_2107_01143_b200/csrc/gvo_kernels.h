@@ -32,7 +32,12 @@ struct PlanShare {
   int64_t cap = 0;
   unsigned long long* n_used = nullptr;
   int64_t* src = nullptr;        // per batch config: slot, -2 - slot (leader) or -1
+  bool defer_rows = false;       // followers' coefficient rows / class tables by launch_plan_rows
+  const uint8_t* need = nullptr; // per batch config: rows needed (a unit computes); null = all
 };
+void launch_plan_rows(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs, int64_t n,
+                      const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos, int64_t* d_ctabs, const PlanShare& PS,
+                      cudaStream_t st);
 __host__ __device__ int64_t plan_slot_words(int64_t max_acc);
 void launch_setup(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs,
                   int64_t n, const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos, int64_t* d_ctabs,
@@ -119,7 +124,8 @@ void launch_dedup(const TplView& T, const gvo_machine* d_machines, const int32_t
 // dedup_units(n, F, S) entries, d_cnt three counters
 void launch_worklists(const TplView& T, const gvo_config* d_cfgs, const Geo* d_geos, int64_t n, int F, int S,
                       const int64_t* d_lead, int wave_field_major, int32_t* d_list, unsigned long long* d_cnt,
-                      const int32_t** wl_wave, const int32_t** wl_blk, const int32_t** wl_warp, cudaStream_t st);
+                      const int32_t** wl_wave, const int32_t** wl_blk, const int32_t** wl_warp, uint8_t* d_need,
+                      cudaStream_t st);
 void launch_dedup_copy(const gvo_config* d_cfgs, const Geo* d_geos, const TplView& T, int64_t* d_counts_all,
                        int64_t counts_stride, int64_t n, int F, int S, int64_t b0, const int64_t* d_lead,
                        int64_t* d_l1_access_all, int32_t l1_stride, cudaStream_t st);

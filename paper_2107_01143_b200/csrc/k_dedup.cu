@@ -247,7 +247,8 @@ void launch_dedup_copy(const gvo_config* d_cfgs, const Geo* d_geos, const TplVie
 // The set kernel re-checks every condition, so the lists only need to be a
 // superset of the computing units.
 __global__ void k_worklist(TplView T, const gvo_config* cfgs, const Geo* geos, int64_t n, int F, int S,
-                           const int64_t* lead, int seg, int wave_fm, int32_t* out, unsigned long long* cnt) {
+                           const int64_t* lead, int seg, int wave_fm, int32_t* out, unsigned long long* cnt,
+                           uint8_t* need) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t total = seg == 0 ? n * F : seg == 1 ? n * F * S : n * (S + 1);
   bool keep = false;
@@ -271,6 +272,7 @@ __global__ void k_worklist(TplView T, const gvo_config* cfgs, const Geo* geos, i
     if (seg == 0) keep = keep && f < nf && phase_ok(G, 1);
     else if (seg == 1) keep = keep && f < nf && phase_ok(G, 0) && j < G.n_samples && G.dup_of[f][j] < 0;
     else keep = keep && (j == S ? phase_ok(G, 2) : phase_ok(G, 0) && j < G.n_samples);
+    if (keep && need) need[c] = 1;  // this configuration's plan rows are read
   }
   const unsigned bal = __ballot_sync(0xffffffffu, keep);
   const int lane = threadIdx.x & 31;
@@ -282,16 +284,18 @@ __global__ void k_worklist(TplView T, const gvo_config* cfgs, const Geo* geos, i
 
 void launch_worklists(const TplView& T, const gvo_config* d_cfgs, const Geo* d_geos, int64_t n, int F, int S,
                       const int64_t* d_lead, int wave_field_major, int32_t* d_list, unsigned long long* d_cnt,
-                      const int32_t** wl_wave, const int32_t** wl_blk, const int32_t** wl_warp, cudaStream_t st) {
+                      const int32_t** wl_wave, const int32_t** wl_blk, const int32_t** wl_warp, uint8_t* d_need,
+                      cudaStream_t st) {
   const int64_t seg_n[3] = {n * F, n * F * S, n * (S + 1)};
   cudaMemsetAsync(d_cnt, 0, 3 * sizeof(unsigned long long), st);
+  if (d_need) cudaMemsetAsync(d_need, 0, (size_t)n, st);
   int32_t* out = d_list;
   const int32_t** dst[3] = {wl_wave, wl_blk, wl_warp};
   for (int seg = 0; seg < 3; ++seg) {
     *dst[seg] = out;
     if (seg_n[seg] > 0)
       k_worklist<<<(unsigned)((seg_n[seg] + 255) / 256), 256, 0, st>>>(T, d_cfgs, d_geos, n, F, S, d_lead, seg,
-                                                                        wave_field_major, out, d_cnt);
+                                                                        wave_field_major, out, d_cnt, d_need);
     out += seg_n[seg];
   }
 }

@@ -558,13 +558,19 @@ __global__ void __launch_bounds__(256) k_setup(TplView T, const gvo_machine* mac
 
 // One CTA per configuration: followers take their leader's plan with the
 // field-base shifts, or compute it when the leader's plan is not shareable.
+// Phase 0: the geometry (what sharing, work lists and the float assembly
+// read) or the whole plan of a follower that computes itself; phase 1 (after
+// the work lists): coefficient rows and class tables, only for followers
+// with a unit that computes (need[c]; null = all) — most followers copy
+// every count from another configuration and never read them.
 __global__ void __launch_bounds__(256) k_plan_follow(TplView T, const gvo_machine* machines, const gvo_config* cfgs,
                                                      int64_t n, gvo_sampling smp, int64_t* coefs, Geo* geos,
-                                                     int64_t* ctabs, PlanShare PS) {
+                                                     int64_t* ctabs, PlanShare PS, int phase) {
   const int64_t c = blockIdx.x;
   if (c >= n) return;
   const int64_t ps = PS.src[c];
   if (ps < 0) return;
+  if (phase == 1 && PS.need && !PS.need[c]) return;
   const int64_t* slot = PS.cache + ps * plan_slot_words(T.max_acc);
   const gvo_config cfg = cfgs[c];
   const int tpl = cfg.template_id;
@@ -583,13 +589,16 @@ __global__ void __launch_bounds__(256) k_plan_follow(TplView T, const gvo_machin
   }
   __syncthreads();
   if (!s_ok) {
-    setup_one(T, machines, cfgs, c, smp, coefs, geos, ctabs, nullptr);
+    if (phase == 0) setup_one(T, machines, cfgs, c, smp, coefs, geos, ctabs, nullptr);
     return;
   }
-  const int words = (int)(sizeof(Geo) / 4);
-  const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(slot + plan_geo_off());
-  uint32_t* gdst = reinterpret_cast<uint32_t*>(geos + c);
-  for (int i = threadIdx.x; i < words; i += blockDim.x) gdst[i] = gsrc[i];
+  if (phase == 0) {
+    const int words = (int)(sizeof(Geo) / 4);
+    const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(slot + plan_geo_off());
+    uint32_t* gdst = reinterpret_cast<uint32_t*>(geos + c);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) gdst[i] = gsrc[i];
+    return;
+  }
   // coefficients: the constant of an affine access moves with its field's base
   const int64_t* csrc = slot + plan_coef_off();
   int64_t* crow = coefs + c * (int64_t)T.max_acc * 8;
@@ -629,9 +638,21 @@ void launch_setup(const TplView& T, const gvo_machine* d_machines, const gvo_con
   }
   k_setup<<<(unsigned)n, 256, setup_smem(T.max_acc), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs, d_geos, d_ctabs,
                                                            PS);
-  if (PS.src)
+  if (PS.src) {
     k_plan_follow<<<(unsigned)n, 256, setup_smem(T.max_acc), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs, d_geos,
-                                                                   d_ctabs, PS);
+                                                                   d_ctabs, PS, 0);
+    if (!PS.defer_rows)
+      k_plan_follow<<<(unsigned)n, 256, setup_smem(T.max_acc), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs, d_geos,
+                                                                     d_ctabs, PS, 1);
+  }
+}
+
+void launch_plan_rows(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs, int64_t n,
+                      const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos, int64_t* d_ctabs, const PlanShare& PS,
+                      cudaStream_t st) {
+  if (n > 0 && PS.src)
+    k_plan_follow<<<(unsigned)n, 256, setup_smem(T.max_acc), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs, d_geos,
+                                                                   d_ctabs, PS, 1);
 }
 
 __global__ void k_classes_only(TplView T, const gvo_config* cfgs, int64_t n, const int64_t* coefs,

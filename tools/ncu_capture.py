@@ -101,9 +101,18 @@ def main():
                       "dram_bytes_per_step": sets["dram"], "dram_bytes_per_launch": sets["dram"] / sets["launches"],
                       "issue_active_pct": sets["issue_w"] / sets["time_s"] if sets["time_s"] else None,
                       "share_of_step_ncu": sets["time_s"] / total_t if total_t else None}}
-    # one full-set capture of the median k_sets launch
+    # one full-set capture of the median k_sets launch that does work (a
+    # batch queues both residencies of the set kernel when the residency is
+    # picked on the device; the other launch exits at once)
     full = out_dir / f"ncu_full_k_sets_{wl.lower()}.csv"
-    skip = max(0, sets["launches"] // 2)
+    set_times = [(lid, mv.get("gpu__time_duration.sum", 0.0)) for (lid, name), mv in sorted(per.items(),
+                 key=lambda kv: int(kv[0][0])) if name.split("(")[0].split("::")[-1] == "k_sets"]
+    real = [i for i, (_, t) in enumerate(set_times) if t > 1e-4]
+    by_t = sorted(real, key=lambda i: set_times[i][1])
+    skip = by_t[len(by_t) // 2] if by_t else max(0, sets["launches"] // 2)
+    cap["k_sets"]["launches_doing_work_per_step"] = len(real)
+    if real:
+        cap["k_sets"]["dram_bytes_per_launch"] = sets["dram"] / len(real)
     r = subprocess.run([NCU, "--set", "full", "--clock-control", "none", "-k", "regex:k_sets", "--launch-skip",
                         str(skip), "--launch-count", "1", "--import-source", "on",
                         "--export", str(out_dir / f"ncu_k_sets_{wl.lower()}"), "--force-overwrite", *bench], cwd=ROOT)
@@ -124,7 +133,8 @@ def main():
                         hw[k] = float(vals[j].replace(",", "")) * SCALE.get(units[j], 1)
                     except ValueError:
                         hw[k] = vals[j]
-            hw["launch"] = f"k_sets launch {skip + 1} of {sets['launches']} in the step"
+            hw["launch"] = (f"k_sets launch {skip + 1} of {sets['launches']} in the step (median duration of the "
+                            f"{len(real)} launches doing work)")
             cap["k_sets"]["hw"] = hw
     dst = ROOT / "profiles" / f"r02_ncu_capture_{wl.lower()}.json"
     dst.write_text(json.dumps(cap, indent=1) + "\n")

@@ -44,3 +44,43 @@ print("ranges", int(ph[:, 8].sum()), "bitmap", int(ph[:, 9].sum()), "sum N", int
 busy = ph[:, 1:8].sum(1) / 1e3
 print("per-CTA fetch-wait kcycles p50/max", np.percentile(ph[:, 0] / 1e3, [50, 100]).round(0),
       "busy kcycles p10/p50/p90/max", np.percentile(busy, [10, 50, 90, 100]).round(0))
+# per-unit statistics of the batch: cycles by (template kind/layout/folding, unit kind)
+st = raw[: n_items.value * 10].reshape(-1, 10)
+F, S = out["F"], out["S"]
+n_cfg = n_items.value // (F * (S + 1))
+from collections import defaultdict  # noqa: E402
+agg = defaultdict(lambda: [0, 0, 0])
+agg_ph = {}
+nr_blk, n_blk = [], []
+for i in np.flatnonzero(st[:, 3] > 0).tolist():
+    if i < n_cfg * F:
+        f, c = divmod(i, n_cfg)  # wave units field-major
+        kind = "wave"
+    else:
+        r = i - n_cfg * F
+        c = r // (F * S); f = (r // S) % F
+        kind = "blk"
+    t = sp.templates[int(sp.tpl[c])]
+    lab = t.label.split("/a")[0] + "/" + t.folding
+    a = agg[(lab, kind, f)]
+    a[0] += int(st[i, 3]); a[1] += 1; a[2] += int(st[i, 1])
+    if kind == "blk":
+        nr_blk.append(int(st[i, 0])); n_blk.append(int(st[i, 1]))
+    ph4 = agg_ph.setdefault(kind, np.zeros(5))
+    ph4[:4] += st[i, 6:10]
+    ph4[4] += st[i, 2]  # in shared memory (not split)
+tot = sum(v[0] for v in agg.values())
+print("unit cycles total G", round(tot / 1e9, 3))
+if n_blk:
+    nb_ = np.array(n_blk); nr_ = np.array(nr_blk)
+    print("CTA-path block units", len(nb_), "N p10/p50/p90", np.percentile(nb_, [10, 50, 90]).tolist(),
+          "runs p10/p50/p90", np.percentile(nr_, [10, 50, 90]).tolist(), "N>512", int((nb_ > 512).sum()),
+          "runs>64", int((nr_ > 64).sum()))
+nrng_ = int(raw[n_items.value * 10])
+rr = raw[n_items.value * 10 + 10: n_items.value * 10 + 10 + min(nrng_, 4096) * 10].reshape(-1, 10)
+bund = rr[rr[:, 8] == 3]
+print("bundles (sampled)", len(bund), "fallbacks in them", int(bund[:, 2].sum()) if len(bund) else 0)
+for k, v in agg_ph.items():
+    print(f"  {k}: runs/emit/sort/sweep Gcyc {np.round(v[:4] / 1e9, 3).tolist()} units in smem {int(v[4])}")
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:20]:
+    print(f"  {k[0]:28s} {k[1]:4s} f{k[2]} units {v[1]:6d} Gcyc {v[0]/1e9:7.3f} ({100*v[0]/tot:4.1f}%) mean kcyc {v[0]/v[1]/1e3:7.1f} mean N {v[2]/v[1]:8.0f}")
