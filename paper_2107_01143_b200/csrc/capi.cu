@@ -510,7 +510,8 @@ static int ensure_work(gvo_ctx* ctx, int64_t n) {
     // leaves some fields unused: defined bytes for initcheck, once
     CK(cudaMemset(ctx->slab.p, 0, (size_t)ctx->slab_bytes * ctx->n_ctas));
   }
-  if (!ctx->status.ensure(4) || !ctx->work.ensure(1)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
+  // work[0] the set kernel's item counter, work[1] its block-unit pool, work[2..3] sharing statistics
+  if (!ctx->status.ensure(4) || !ctx->work.ensure(4)) return set_err(ctx, GVO_ERR_CUDA, "alloc failed%s");
   if (!ctx->split) {
     const size_t hdr = 256;
     const size_t qb = (size_t)ctx->split_qcap * sizeof(RangeItem);

@@ -1971,6 +1971,9 @@ struct SetsArgs {
 // own shared-memory slice, bitonic-sorts them in place (the sweep needs key
 // order only, not stability) and sweeps.  Units that do not fit fall back to
 // the CTA path.
+#ifndef GVO_BLOCK_POOL
+#define GVO_BLOCK_POOL 0  // A/B: 1 = warp-scheduled block-unit pool (C5 stencil part 330 vs 312 ms: rejected)
+#endif
 constexpr int kMicroElems = 512;
 constexpr int kMicroRuns = 64;          // run offsets kept per warp
 constexpr int kMicroRunCap = 256;       // runs per warp in the global slab
@@ -2380,11 +2383,26 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       continue;
     }
     if (!in_range && micro_on && item >= n_wave_u && item < n_set_main) {
-      // bundle of kNW block units, one per warp
+      // block units, one per warp: the bundle's kNW units.  A/B
+      // GVO_BLOCK_POOL=1: a bundle item lets the CTA join a block-unit pool
+      // (every warp takes units from a global counter until it is drained,
+      // no CTA barrier between units) — slower on C5 (330 vs 312 ms for the
+      // stencil part): the CTAs in the pool stop taking queued key ranges
+      // and CTA-path fallbacks, which then pile up in the tail.
       const int w = threadIdx.x >> 5;
-      int64_t bidx = (item - n_wave_u) * kNW + w;
-      if (use_wl) bidx = bidx < n_blk_l ? P.wl_blk[bidx] : n_blk_u;
-      if (bidx < n_blk_u) {
+#if GVO_BLOCK_POOL
+      for (;;) {
+        unsigned long long v = 0;
+        if ((threadIdx.x & 31) == 0) v = atomicAdd(P.work + 1, 1ull);
+        v = __shfl_sync(0xffffffffu, v, 0);
+        if ((int64_t)v >= n_blk_l) break;
+        const int64_t bidx = use_wl ? (int64_t)P.wl_blk[v] : (int64_t)v;
+#else
+      for (int once = 0; once < 1; ++once) {
+        int64_t bidx = (item - n_wave_u) * kNW + w;
+        if (use_wl) bidx = bidx < n_blk_l ? P.wl_blk[bidx] : n_blk_u;
+        if (bidx >= n_blk_u) break;
+#endif
         const bool ok = micro_unit(P, bidx, micro_region + w * kMicroBytes, cpts + w * kClassPts,
                                    runs + w * kMicroRunCap);
         if (!ok && (threadIdx.x & 31) == 0) {
@@ -2406,8 +2424,18 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
               atomicAdd(&SS->pending, ~0ull);
             }
           }
-          if (!queued) fb_list[atomicAdd(&fb_n, 1)] = bidx;
+          if (!queued) {
+            const int q = atomicAdd(&fb_n, 1);
+            if (q < kNW) {
+              fb_list[q] = bidx;
+            } else {  // local list full too: the configuration fails loudly
+              atomicSub(&fb_n, 1);
+              int64_t* row = P.counts + (bidx / ((int64_t)P.F_stride * P.S_req)) * P.counts_stride;
+              atomicExch((unsigned long long*)&row[GVO_C_STATUS], (unsigned long long)GVO_ERR_CAPACITY);
+            }
+          }
         }
+        __syncwarp();
       }
       __syncthreads();
       if (threadIdx.x == 0 && P.unit_stats && SS) {
@@ -3305,7 +3333,7 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st) {
   P.wave_field_major = L.wave_field_major;
   P.epoch = L.epoch;  // never 0 (the zeroed initial state), unique per launch
   if (P.n_items + P.n_warp_items <= 0) return;
-  cudaMemsetAsync(P.work, 0, sizeof(unsigned long long), st);
+  cudaMemsetAsync(P.work, 0, 2 * sizeof(unsigned long long), st);  // item counter, block-unit pool
   // head, tail, pending (descriptor slots are all free again when a launch ends)
   if (P.split) cudaMemsetAsync(P.split, 0, 4 * sizeof(unsigned long long), st);
   static bool attr = false;
