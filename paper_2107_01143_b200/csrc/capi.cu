@@ -97,6 +97,7 @@ struct gvo_ctx {
   DBuf<uint8_t> plan_need;
   // work lists of the set kernel (k_dedup.cu k_worklist), per batch
   bool worklist = true;
+  int64_t handoff_min = 1024;  // batches from this size hand large block units to the CTA (GVO_HANDOFF_MIN)
   DBuf<int32_t> wl_list;
   DBuf<unsigned long long> wl_cnt;
   DBuf<DedupEntry> dd_table;
@@ -302,6 +303,7 @@ int gvo_open(int device, gvo_ctx** out) {
   if (const char* e = getenv("GVO_DEDUP")) ctx->dedup = atoi(e) != 0;
   if (const char* e = getenv("GVO_PLAN_SHARE")) ctx->plan_share = atoi(e) != 0;
   if (const char* e = getenv("GVO_WORKLIST")) ctx->worklist = atoi(e) != 0;
+  if (const char* e = getenv("GVO_HANDOFF_MIN")) ctx->handoff_min = atoll(e);
   ctx->n_ctas = kMaxSetsCtasPerSm * ctx->n_sm;
   *out = ctx;
   return GVO_OK;
@@ -671,6 +673,7 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
     L.pat_off = ctx->pat_off;
     L.wave_field_major = ctx->wave_fm;
     L.lead = lead;
+    L.handoff = nb >= ctx->handoff_min ? 1 : 0;
     if (ctx->worklist && S > 0) {
       if (!ctx->wl_list.ensure((size_t)dedup_units(nb, F, S)) || !ctx->wl_cnt.ensure(3))
         return set_err(ctx, GVO_ERR_CUDA, "work list alloc failed%s");

@@ -93,6 +93,7 @@ struct SetsLaunch {
   // residency chosen on the device: the launch runs only if *run_if == run_if_val
   const int* run_if = nullptr;
   int run_if_val = 0;
+  int handoff = 0;  // micro-tier handoffs of large block units to the CTA (large batches)
 };
 // *d_flag = 0 iff every config of the batch has a template with >= 3 fields (else 1)
 void launch_batch_wide(const TplView& T, const gvo_config* d_cfgs, int64_t n, int* d_flag, cudaStream_t st);

@@ -1962,6 +1962,7 @@ struct SetsArgs {
   const unsigned long long* wl_cnt;
   const int* run_if;        // residency picked on the device: run only if *run_if == run_if_val
   int run_if_val;
+  int handoff;              // micro handoffs on (large batches)
 };
 
 // ------------------------------------------------------------------ micro tier
@@ -1977,9 +1978,14 @@ struct SetsArgs {
 constexpr int kMicroElems = 512;
 constexpr int kMicroRuns = 64;          // run offsets kept per warp
 constexpr int kMicroRunCap = 256;       // runs per warp in the global slab
+struct Handoff {
+  int64_t bidx, N, key_lo, key_hi;
+  int w, nr;
+};
 struct MicroCnt {
   int n_runs, status;
   int64_t key_lo, key_hi;
+  int64_t N;  // intervals of a handoff
 };
 constexpr int kMicroBytes = (int)(((sizeof(MicroCnt) + 15) & ~15) + (kMicroRuns + 1) * 8 + kMicroElems * 8);
 
@@ -2008,7 +2014,41 @@ __device__ __forceinline__ void warp_bitonic(uint64_t* a, int p) {
 }
 
 // returns false when the unit must be processed by the whole CTA
-__device__ bool micro_unit(const SetsArgs& P, int64_t bidx, uint8_t* reg, int64_t* wpts, Run* wruns) {
+// Micro units whose intervals or runs exceed the warp's slice take their
+// element buffer / run offsets from the CTA's overflow pool (the shared
+// memory beyond the micro slices, bump-allocated per bundle) instead of
+// falling back to the CTA path, which would build the runs again with 2 of
+// its 10 warps busy (C5: those fallbacks were ~23 % of a stencil batch).
+#ifndef GVO_MICRO_POOL
+#define GVO_MICRO_POOL 0  // A/B (rejected: a warp on a large unit holds its bundle; C2 0.42 -> 1.03 ms, C5 LBM 169 -> 199 ms)
+#endif
+struct MicroPool {
+  uint8_t* base;
+  uint32_t bytes;
+  unsigned int* used;
+};
+
+__device__ __forceinline__ void* micro_alloc(const MicroPool& M, uint32_t bytes) {
+  const int lane = threadIdx.x & 31;
+  bytes = (bytes + 15u) & ~15u;
+  unsigned int off = 0;
+  if (lane == 0) off = M.used ? atomicAdd(M.used, bytes) : ~0u;
+  off = __shfl_sync(0xffffffffu, off, 0);
+  if (!M.used || off > M.bytes || bytes > M.bytes - off) return nullptr;
+  return M.base + off;
+}
+
+// Returns 1 when the unit is done, 0 when the CTA path must process it from
+// scratch, 2 when its runs are built (wruns, metadata in the warp's
+// MicroCnt) but its intervals exceed the warp's slice: the CTA emits, sorts
+// and sweeps them after the bundle (handoff, GVO_MICRO_HANDOFF) instead of
+// building the runs again with the 2 of 10 warps a block unit's few lattice
+// tasks keep busy.
+#ifndef GVO_MICRO_HANDOFF
+#define GVO_MICRO_HANDOFF 1
+#endif
+__device__ int micro_unit(const SetsArgs& P, int64_t bidx, uint8_t* reg, int64_t* wpts, Run* wruns,
+                          const MicroPool& pool) {
   const int lane = threadIdx.x & 31;
   const int F = P.F_stride, S = P.S_req;
   const int64_t c = bidx / ((int64_t)F * S);
@@ -2017,8 +2057,8 @@ __device__ bool micro_unit(const SetsArgs& P, int64_t bidx, uint8_t* reg, int64_
   const Geo& G = P.geos[c];
   const gvo_config cfg = P.cfgs[c];
   const int tpl = cfg.template_id;
-  if (f >= P.T.n_fields[tpl] || !phase_ok(G, 0) || j >= G.n_samples || G.dup_of[f][j] >= 0) return true;
-  if (P.lead && P.lead[(int64_t)F * (P.n_items / ((int64_t)F * (S + 1))) + bidx] >= 0) return true;
+  if (f >= P.T.n_fields[tpl] || !phase_ok(G, 0) || j >= G.n_samples || G.dup_of[f][j] >= 0) return 1;
+  if (P.lead && P.lead[(int64_t)F * (P.n_items / ((int64_t)F * (S + 1))) + bidx] >= 0) return 1;
   MicroCnt* cnt = reinterpret_cast<MicroCnt*>(reg);
   int64_t* roff = reinterpret_cast<int64_t*>(reg + ((sizeof(MicroCnt) + 15) & ~size_t(15)));
   uint64_t* el = reinterpret_cast<uint64_t*>(roff + kMicroRuns + 1);
@@ -2085,7 +2125,28 @@ __device__ bool micro_unit(const SetsArgs& P, int64_t bidx, uint8_t* reg, int64_
   }
   __syncwarp();
   const int nr = cnt->n_runs;
-  if (cnt->status != GVO_OK || nr > kMicroRuns) return false;
+  if (cnt->status != GVO_OK) return 0;
+#if GVO_MICRO_HANDOFF
+  {
+    int64_t nl = 0;
+    for (int r = lane; r < nr; r += 32) nl += wruns[r].count;
+    for (int o = 16; o; o >>= 1) nl += __shfl_xor_sync(0xffffffffu, nl, o);
+    if (nr > kMicroRuns || nl > kMicroElems) {
+      const int64_t kb = nr ? floordiv(cnt->key_lo, R) * R : 0;
+      if (nl > P.elem_cap || nr > kMicroRunCap ||
+          (nr && (uint64_t)(cnt->key_hi - kb) >= (uint64_t(1) << kKeyBits)))
+        return 0;
+      if (lane == 0) cnt->N = nl;
+      __syncwarp();
+      return 2;
+    }
+  }
+#endif
+  if (nr > kMicroRuns) {  // run offsets from the overflow pool
+    if (!GVO_MICRO_POOL || nr > kMicroRunCap) return 0;
+    roff = reinterpret_cast<int64_t*>(micro_alloc(pool, (uint32_t)(nr + 1) * 8u));
+    if (!roff) return 0;
+  }
   // offsets
   if (lane == 0) {
     int64_t acc = 0;
@@ -2095,9 +2156,14 @@ __device__ bool micro_unit(const SetsArgs& P, int64_t bidx, uint8_t* reg, int64_
   __syncwarp();
   const int64_t N = roff[nr];
   const int64_t kbase = nr ? floordiv(cnt->key_lo, R) * R : 0;
-  if (N > kMicroElems || (nr && (uint64_t)(cnt->key_hi - kbase) >= (uint64_t(1) << kKeyBits))) return false;
+  if (nr && (uint64_t)(cnt->key_hi - kbase) >= (uint64_t(1) << kKeyBits)) return 0;
   int p = 32;
   while (p < N) p <<= 1;
+  if (N > kMicroElems) {  // element buffer from the overflow pool
+    if (!GVO_MICRO_POOL || N > (int64_t)(pool.bytes / 8)) return 0;
+    el = reinterpret_cast<uint64_t*>(micro_alloc(pool, (uint32_t)p * 8u));
+    if (!el) return 0;
+  }
   const int64_t tpb = G.tpb;
   for (int64_t i = lane; i < p; i += 32) {
     if (i >= N) { el[i] = ~0ull; continue; }
@@ -2163,7 +2229,7 @@ __device__ bool micro_unit(const SetsArgs& P, int64_t bidx, uint8_t* reg, int64_
     b[3] = res[2];
   }
   __syncwarp();
-  return true;
+  return 1;
 }
 
 // Write a finished unit's measures (union counts per subset) to the outputs.
@@ -2244,6 +2310,14 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
   GVO_PH(__shared__ long long ph[16];)
   GVO_PH(if (threadIdx.x < 16) ph[threadIdx.x] = 0;)
   if (threadIdx.x == 0) { main_done = 0; fb_n = 0; fb_i = 0; }
+  // micro overflow pool: the shared memory beyond the micro slices (reset per bundle at fetch)
+  __shared__ unsigned int pool_used;
+  // micro handoffs of the current bundle (reset at fetch)
+  __shared__ Handoff ho[kNW];
+  __shared__ int ho_n;
+  const size_t pool_off = ((size_t)(micro_region - smem) + (size_t)kNW * kMicroBytes + 15) & ~size_t(15);
+  const MicroPool mpool{smem + pool_off, (uint32_t)(kSetsSmemBytes > (int)pool_off ? kSetsSmemBytes - pool_off : 0),
+                        &pool_used};
   // item space (mode 0): wave units | bundles of kNW block units (micro) | warp items;
   // block units falling back to the CTA path re-enter as kBlkBase + index
   const bool micro_on = P.mode == 0 && P.S_req > 0;
@@ -2343,6 +2417,8 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         __nanosleep(256);
       }
       next_kind = kind;
+      pool_used = 0;
+      ho_n = 0;
       next_item = it;
     }
     __syncthreads();
@@ -2365,6 +2441,129 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
     SplitHdr* hdr = nullptr;
     bool in_range = kind_fetched == 1;
     const long long t_start = clock64();
+    // emission + sort + sweeps + outputs of an unsplit unit described by U,
+    // runs urun[0, U.n_runs) with offsets roff: the CTA path's units and the
+    // micro tier's handoffs (runs built by one warp, too many intervals for
+    // its slice)
+    auto finish_unsplit = [&](const Run* urun, int64_t* roff) {
+      const int64_t c = U.cfg;
+      const Geo& G = P.geos[c];
+      const gvo_config cfg = P.cfgs[c];
+      const int tpl = cfg.template_id;
+      const int abase = P.T.acc_base[tpl];
+      const int64_t* fbase = P.T.field_base + P.T.field_base_off[tpl];
+      const int32_t bd[3] = {cfg.block[0], cfg.block[1], cfg.block[2]};
+      const int64_t gd[3] = {cfg.grid[0], cfg.grid[1], cfg.grid[2]};
+      const Granule Gr = Granule::make(U.g);
+      const int64_t tpb = G.tpb;
+      const int nr = min(U.n_runs, (int)P.run_cap);
+      const long long t_runs = t_runs_sh;
+    const int64_t N = U.N;
+      uint64_t* A0;
+      uint64_t* B0;
+      if (N <= sm_elems) { A0 = ebuf; B0 = ebuf + sm_elems; }
+      else { A0 = gbuf; B0 = gbuf + P.elem_cap; }
+      const int64_t kbase = U.key_lo;
+
+      // ---------------- emission: each thread owns a contiguous element range
+      // (one binary search for its first run, then a cursor), outer-tuple
+      // decode in 32-bit arithmetic when the run's extents allow it.
+      {
+        const int64_t per = (N + kNT - 1) / kNT;
+        const int64_t e0 = min(N, (int64_t)threadIdx.x * per), e1 = min(N, e0 + per);
+        int ri = 0;
+        if (e0 < e1) {
+          int lo = 0, hi = nr - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (roff[mid] <= e0) lo = mid; else hi = mid - 1;
+          }
+          ri = lo;
+        }
+        for (int64_t i = e0; i < e1; ++i) {
+          while (roff[ri + 1] <= i) ++ri;
+          const Run& r = urun[ri];
+          int64_t k = i - roff[ri];
+          int64_t glo, ghi;
+          if (r.kind == 0) {
+            int64_t piece = 0;
+            if (r.pieces > 1) { piece = k % r.pieces; k /= r.pieces; }
+            uint64_t b = (uint64_t)r.base;
+            if (k < (int64_t(1) << 31)) {
+              uint32_t k32 = (uint32_t)k;
+              for (int d = r.nd - 1; d >= 0; --d) {
+                const uint32_t ex = (uint32_t)r.ext[d];
+                const uint32_t q = ex ? k32 / ex : 0;
+                b += (uint64_t)r.stride[d] * (uint64_t)(k32 - q * ex);
+                k32 = q;
+              }
+            } else {
+              for (int d = r.nd - 1; d >= 0; --d) {
+                const int64_t idx = k % r.ext[d];
+                k /= r.ext[d];
+                b += (uint64_t)r.stride[d] * (uint64_t)idx;
+              }
+            }
+            glo = Gr.of((int64_t)b);
+            ghi = Gr.of((int64_t)(b + r.span));
+            if (r.pieces > 1) {
+              int64_t plo = glo + piece * kPiece;
+              if (plo > ghi) plo = glo;
+              const int64_t phi = min(ghi, plo + kPiece - 1);
+              glo = plo;
+              ghi = phi;
+            }
+          } else {
+            const int64_t blk = r.run_start + k / tpb;
+            const int64_t th = k % tpb;
+            int64_t crd[6];
+            crd[0] = th % bd[0];
+            crd[1] = (th / bd[0]) % bd[1];
+            crd[2] = th / ((int64_t)bd[0] * bd[1]);
+            crd[3] = blk % gd[0];
+            crd[4] = (blk / gd[0]) % gd[1];
+            crd[5] = blk / (gd[0] * gd[1]);
+            const int ga = abase + r.access;
+            glo = ghi = Gr.of(eval_point(P.T.code + P.T.code_off[ga], P.T.code_len[ga], crd, bd, fbase));
+          }
+          A0[i] = ((uint64_t)(glo - kbase) << kKeyShift) | ((uint64_t)(ghi - glo) << kTagBits) |
+                  (uint64_t)r.tag;
+        }
+      }
+      __syncthreads();
+
+      const long long t_emit = clock64();
+      // ---------------- sort + sweeps
+      int kb = 0;
+      {
+        uint64_t span = (uint64_t)(U.key_hi - kbase);
+        while (span) { ++kb; span >>= 1; }
+      }
+      const int nbits = ((kb + 7) / 8) * 8;
+      const uint64_t* sorted = cta_sort(A0, B0, N, kKeyShift, nbits, hist, tot);
+      const long long t_sort = clock64();
+      sweep(sorted, N, U, wmax);
+      const long long t_sweep = clock64();
+      GVO_PH(if (threadIdx.x == 0) ph[4] += t_sweep - t_runs;)
+
+      // ---------------- outputs
+      if (threadIdx.x == 0 && P.unit_stats) {
+        int64_t* us = P.unit_stats + stat_idx * 10;
+        us[6] = t_runs - t_start;
+        us[7] = t_emit - t_runs;
+        us[8] = t_sort - t_emit;
+        us[9] = t_sweep - t_sort;
+        us[0] = nr;
+        us[1] = N;
+        us[2] = N <= sm_elems;
+        us[3] = clock64() - t_start;
+        us[4] = nbits;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        us[5] = smid;
+      }
+      if (threadIdx.x == 0) write_unit_outputs(P, c, U.field, U.kind, U.j, P.mode == 2 ? 0 : G.n_uw, U.sub_val);
+    };
 
     if (!in_range && item >= n_set_main && item < kBlkBase) {
 #if defined(GVO_DEBUG_SYNC) && GVO_DEBUG_SYNC
@@ -2403,9 +2602,23 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         if (use_wl) bidx = bidx < n_blk_l ? P.wl_blk[bidx] : n_blk_u;
         if (bidx >= n_blk_u) break;
 #endif
-        const bool ok = micro_unit(P, bidx, micro_region + w * kMicroBytes, cpts + w * kClassPts,
-                                   runs + w * kMicroRunCap);
-        if (!ok && (threadIdx.x & 31) == 0) {
+        const int res0 = micro_unit(P, bidx, micro_region + w * kMicroBytes, cpts + w * kClassPts,
+                                    runs + w * kMicroRunCap, mpool);
+        // the pool has no per-bundle handoff list; small batches spread the
+        // large units over idle CTAs through the queue instead (C2: 0.45 vs
+        // 0.56 ms with handoffs)
+        const int res = (GVO_BLOCK_POOL || !P.handoff) && res0 == 2 ? 0 : res0;
+        if (res == 2 && (threadIdx.x & 31) == 0) {  // runs built: the CTA finishes it after the bundle
+          const MicroCnt* mc = reinterpret_cast<const MicroCnt*>(micro_region + w * kMicroBytes);
+          Handoff& H = ho[atomicAdd(&ho_n, 1)];
+          H.bidx = bidx;
+          H.N = mc->N;
+          H.key_lo = mc->key_lo;
+          H.key_hi = mc->key_hi;
+          H.w = w;
+          H.nr = mc->n_runs;
+        }
+        if (res == 0 && (threadIdx.x & 31) == 0) {
           bool queued = false;
           if (SS) {
             atomicAdd(&SS->pending, 1ull);
@@ -2438,6 +2651,60 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         __syncwarp();
       }
       __syncthreads();
+      // handoffs: units whose runs a warp built but whose intervals exceed
+      // its slice — emission, sort, sweep and outputs by the whole CTA
+      for (int h = 0; h < ho_n; ++h) {
+        const int hnr = ho[h].nr;
+        const Run* urun = runs + ho[h].w * kMicroRunCap;
+        if (threadIdx.x == 0) {
+          const Handoff& H = ho[h];
+          const int64_t c = H.bidx / ((int64_t)P.F_stride * P.S_req);
+          const gvo_machine& mach = P.machines[P.cfgs[c].machine_id];
+          const int64_t R = mach.l1_line_bytes / mach.sector_bytes;
+          U.cfg = c;
+          U.field = (int)((H.bidx / P.S_req) % P.F_stride);
+          U.j = (int)(H.bidx % P.S_req);
+          U.kind = 0;
+          U.status = GVO_OK;
+          U.n_runs = hnr;
+          U.N = H.N;
+          U.g = mach.sector_bytes;
+          U.R = R;
+          U.key_lo = hnr ? floordiv(H.key_lo, R) * R : 0;
+          U.key_hi = H.key_hi;
+          U.n_sub = 3;
+          U.sub_mask[0] = 1; U.sub_r[0] = 1;  // load sectors
+          U.sub_mask[1] = 1; U.sub_r[1] = R;  // load lines
+          U.sub_mask[2] = 2; U.sub_r[2] = 1;  // store sectors
+          for (int q = 0; q < 3; ++q) {
+            const int64_t r = U.sub_r[q];
+            int sh = -1;
+            if (r > 0 && (r & (r - 1)) == 0) { sh = 0; while ((int64_t(1) << sh) < r) ++sh; }
+            U.sub_sh[q] = sh;
+          }
+          stat_idx = n_wave_u + H.bidx;
+          t_runs_sh = clock64();
+        }
+        // run offsets (<= kMicroRunCap runs): exclusive scan by warp 0
+        if (threadIdx.x < 32) {
+          int64_t carry = 0;
+          for (int r0 = 0; r0 < hnr; r0 += 32) {
+            const int r = r0 + (int)threadIdx.x;
+            const int64_t v = r < hnr ? urun[r].count : 0;
+            int64_t inc = v;
+            for (int o = 1; o < 32; o <<= 1) {
+              const int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+              if ((int)threadIdx.x >= o) inc += t;
+            }
+            if (r < hnr) roff_sh[r] = carry + inc - v;
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+          }
+          if (threadIdx.x == 0) roff_sh[hnr] = carry;
+        }
+        __syncthreads();
+        finish_unsplit(urun, roff_sh);
+        __syncthreads();
+      }
       if (threadIdx.x == 0 && P.unit_stats && SS) {
         const unsigned long long slot =
             atomicAdd(reinterpret_cast<unsigned long long*>(P.unit_stats + P.n_items * 10), 1ull);
@@ -3164,127 +3431,9 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
 
     // ================= unsplit unit: one sort in shared (or slab) memory =================
     {
-      const int64_t c = U.cfg;
-      const Geo& G = P.geos[c];
-      const gvo_config cfg = P.cfgs[c];
-      const int tpl = cfg.template_id;
-      const int abase = P.T.acc_base[tpl];
-      const int64_t* fbase = P.T.field_base + P.T.field_base_off[tpl];
-      const int32_t bd[3] = {cfg.block[0], cfg.block[1], cfg.block[2]};
-      const int64_t gd[3] = {cfg.grid[0], cfg.grid[1], cfg.grid[2]};
-      const Granule Gr = Granule::make(U.g);
-      const int64_t tpb = G.tpb;
-      const int nr = min(U.n_runs, (int)P.run_cap);
-      int64_t* roff = nr <= kSmemRuns ? roff_sh : roff_gl;
-      const long long t_runs = t_runs_sh;
-    const int64_t N = U.N;
-      uint64_t* A0;
-      uint64_t* B0;
-      if (N <= sm_elems) { A0 = ebuf; B0 = ebuf + sm_elems; }
-      else { A0 = gbuf; B0 = gbuf + P.elem_cap; }
-      const int64_t kbase = U.key_lo;
-
-      // ---------------- emission: each thread owns a contiguous element range
-      // (one binary search for its first run, then a cursor), outer-tuple
-      // decode in 32-bit arithmetic when the run's extents allow it.
-      {
-        const int64_t per = (N + kNT - 1) / kNT;
-        const int64_t e0 = min(N, (int64_t)threadIdx.x * per), e1 = min(N, e0 + per);
-        int ri = 0;
-        if (e0 < e1) {
-          int lo = 0, hi = nr - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (roff[mid] <= e0) lo = mid; else hi = mid - 1;
-          }
-          ri = lo;
-        }
-        for (int64_t i = e0; i < e1; ++i) {
-          while (roff[ri + 1] <= i) ++ri;
-          const Run& r = runs[ri];
-          int64_t k = i - roff[ri];
-          int64_t glo, ghi;
-          if (r.kind == 0) {
-            int64_t piece = 0;
-            if (r.pieces > 1) { piece = k % r.pieces; k /= r.pieces; }
-            uint64_t b = (uint64_t)r.base;
-            if (k < (int64_t(1) << 31)) {
-              uint32_t k32 = (uint32_t)k;
-              for (int d = r.nd - 1; d >= 0; --d) {
-                const uint32_t ex = (uint32_t)r.ext[d];
-                const uint32_t q = ex ? k32 / ex : 0;
-                b += (uint64_t)r.stride[d] * (uint64_t)(k32 - q * ex);
-                k32 = q;
-              }
-            } else {
-              for (int d = r.nd - 1; d >= 0; --d) {
-                const int64_t idx = k % r.ext[d];
-                k /= r.ext[d];
-                b += (uint64_t)r.stride[d] * (uint64_t)idx;
-              }
-            }
-            glo = Gr.of((int64_t)b);
-            ghi = Gr.of((int64_t)(b + r.span));
-            if (r.pieces > 1) {
-              int64_t plo = glo + piece * kPiece;
-              if (plo > ghi) plo = glo;
-              const int64_t phi = min(ghi, plo + kPiece - 1);
-              glo = plo;
-              ghi = phi;
-            }
-          } else {
-            const int64_t blk = r.run_start + k / tpb;
-            const int64_t th = k % tpb;
-            int64_t crd[6];
-            crd[0] = th % bd[0];
-            crd[1] = (th / bd[0]) % bd[1];
-            crd[2] = th / ((int64_t)bd[0] * bd[1]);
-            crd[3] = blk % gd[0];
-            crd[4] = (blk / gd[0]) % gd[1];
-            crd[5] = blk / (gd[0] * gd[1]);
-            const int ga = abase + r.access;
-            glo = ghi = Gr.of(eval_point(P.T.code + P.T.code_off[ga], P.T.code_len[ga], crd, bd, fbase));
-          }
-          A0[i] = ((uint64_t)(glo - kbase) << kKeyShift) | ((uint64_t)(ghi - glo) << kTagBits) |
-                  (uint64_t)r.tag;
-        }
-      }
-      __syncthreads();
-
-      const long long t_emit = clock64();
-      // ---------------- sort + sweeps
-      int kb = 0;
-      {
-        uint64_t span = (uint64_t)(U.key_hi - kbase);
-        while (span) { ++kb; span >>= 1; }
-      }
-      const int nbits = ((kb + 7) / 8) * 8;
-      const uint64_t* sorted = cta_sort(A0, B0, N, kKeyShift, nbits, hist, tot);
-      const long long t_sort = clock64();
-      sweep(sorted, N, U, wmax);
-      const long long t_sweep = clock64();
-      GVO_PH(if (threadIdx.x == 0) ph[4] += t_sweep - t_runs;)
-
-      // ---------------- outputs
-      if (threadIdx.x == 0 && P.unit_stats) {
-        int64_t* us = P.unit_stats + stat_idx * 10;
-        us[6] = t_runs - t_start;
-        us[7] = t_emit - t_runs;
-        us[8] = t_sort - t_emit;
-        us[9] = t_sweep - t_sort;
-        us[0] = nr;
-        us[1] = N;
-        us[2] = N <= sm_elems;
-        us[3] = clock64() - t_start;
-        us[4] = nbits;
-        unsigned smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        us[5] = smid;
-      }
-      if (threadIdx.x == 0) {
-        write_unit_outputs(P, c, U.field, U.kind, U.j, P.mode == 2 ? 0 : G.n_uw, U.sub_val);
-        if (SS) atomicAdd(&SS->pending, ~0ull);
-      }
+      const int nr_u = min(U.n_runs, (int)P.run_cap);
+      finish_unsplit(runs, nr_u <= kSmemRuns ? roff_sh : roff_gl);
+      if (threadIdx.x == 0 && SS) atomicAdd(&SS->pending, ~0ull);
       __syncthreads();
     }
   }
@@ -3330,6 +3479,7 @@ void launch_sets(const SetsLaunch& L, cudaStream_t st) {
   P.wl_cnt = L.wl_cnt;
   P.run_if = L.run_if;
   P.run_if_val = L.run_if_val;
+  P.handoff = L.handoff;
   P.wave_field_major = L.wave_field_major;
   P.epoch = L.epoch;  // never 0 (the zeroed initial state), unique per launch
   if (P.n_items + P.n_warp_items <= 0) return;
