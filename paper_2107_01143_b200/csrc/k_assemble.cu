@@ -392,6 +392,20 @@ __global__ void __launch_bounds__(32 * kFinishWarps) k_finish(TplView T, const g
   for (int64_t i = lane; i < stride; i += 32) grow[i] = srow[i];
 }
 
+// thread per config (GVO_FINISH_THREAD, default): the float code is serial
+// per configuration; the warp-per-config form keeps 31 of 32 lanes idle
+// while lane 0 runs it — here every lane runs one configuration, reading its
+// counts row and plan straight from global memory
+__global__ void __launch_bounds__(128) k_finish_t(TplView T, const gvo_machine* machines, const gvo_config* cfgs,
+                                                  const Geo* geos, int64_t n, int S_req, int W_req, int F,
+                                                  int64_t* counts, int64_t stride, double* stats, double* records,
+                                                  double* field_down) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const gvo_config cfg = cfgs[c];
+  finish_one(T, machines, cfg, geos[c], c, S_req, W_req, F, counts + c * stride, stats, records, field_down);
+}
+
 // injected float stats (uniform stride F) -> record
 __global__ void k_assemble_stats(const gvo_machine* machines, const int32_t* mid, const int64_t* flops,
                                  int64_t n, int F, const double* stats, double* records,
@@ -411,6 +425,15 @@ void launch_finish(const TplView& T, const gvo_machine* d_machines, const gvo_co
                    int64_t counts_stride, double* d_stats, double* d_records, double* d_field_down,
                    cudaStream_t st) {
   if (n <= 0) return;
+#ifndef GVO_FINISH_THREAD
+#define GVO_FINISH_THREAD 1
+#endif
+  if (GVO_FINISH_THREAD) {
+    k_finish_t<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(T, d_machines, d_cfgs, d_geos, n, S_req, W_req, F,
+                                                             d_counts, counts_stride, d_stats, d_records,
+                                                             d_field_down);
+    return;
+  }
   const size_t smem = kFinishWarps * (counts_stride + (sizeof(Geo) + 7) / 8) * sizeof(int64_t);
   k_finish<<<(unsigned)((n + kFinishWarps - 1) / kFinishWarps), 32 * kFinishWarps, smem, st>>>(
       T, d_machines, d_cfgs, d_geos, n, S_req, W_req, F, d_counts, counts_stride, d_stats, d_records,
