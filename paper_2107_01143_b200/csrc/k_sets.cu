@@ -2653,7 +2653,8 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
       __syncthreads();
       // handoffs: units whose runs a warp built but whose intervals exceed
       // its slice — emission, sort, sweep and outputs by the whole CTA
-      for (int h = 0; h < ho_n; ++h) {
+      const int nho = ho_n;
+      for (int h = 0; h < nho; ++h) {
         const int hnr = ho[h].nr;
         const Run* urun = runs + ho[h].w * kMicroRunCap;
         if (threadIdx.x == 0) {
@@ -2705,6 +2706,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         finish_unsplit(urun, roff_sh);
         __syncthreads();
       }
+      __syncthreads();  // every thread has read ho_n before the next fetch resets it
       if (threadIdx.x == 0 && P.unit_stats && SS) {
         const unsigned long long slot =
             atomicAdd(reinterpret_cast<unsigned long long*>(P.unit_stats + P.n_items * 10), 1ull);
