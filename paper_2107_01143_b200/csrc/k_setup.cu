@@ -16,6 +16,8 @@
 #include "gvo_bytecode.cuh"
 #include "gvo_kernels.h"
 
+#include <algorithm>
+
 namespace gvo {
 
 __device__ inline void interior(int64_t e, int64_t* off, int64_t* n) {
@@ -241,7 +243,47 @@ __host__ __device__ inline int64_t plan_coef_off() { return plan_geo_off() + ((i
 __host__ __device__ inline int64_t plan_ctab_off(int64_t A) { return plan_coef_off() + A * 8; }
 }  // namespace
 
-__host__ __device__ int64_t plan_slot_words(int64_t max_acc) { return plan_ctab_off(max_acc) + ctab_stride(max_acc); }
+// slots start on 16-byte boundaries (TMA bulk copies of their Geo and coefficient rows)
+__host__ __device__ int64_t plan_slot_words(int64_t max_acc) {
+  return (plan_ctab_off(max_acc) + ctab_stride(max_acc) + 1) & ~int64_t(1);
+}
+
+// ---- TMA (cp.async.bulk) 1D copies through shared memory: the bulk-copy
+// engine moves a follower's geometry and coefficient row (contiguous, 16-byte
+// aligned, 1.1 KB and 64*A bytes) while the threads only patch constants
+#ifndef GVO_PLAN_TMA
+#define GVO_PLAN_TMA 1
+#endif
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void tma_bar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+// global -> shared, completion counted on bar (one thread)
+__device__ __forceinline__ void tma_load_1d(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  }
+}
+// shared -> global (one thread), after the shared-memory writes are fenced to the async proxy
+__device__ __forceinline__ void tma_store_1d(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_store_commit_wait() {
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
 
 // One thread per configuration of the batch: src[c] = slot >= 0 (take the
 // plan cached in slot), -2 - slot (leader: compute, then fill slot), -1
@@ -592,6 +634,36 @@ __global__ void __launch_bounds__(256) k_plan_follow(TplView T, const gvo_machin
     if (phase == 0) setup_one(T, machines, cfgs, c, smp, coefs, geos, ctabs, nullptr);
     return;
   }
+#if GVO_PLAN_TMA
+  extern __shared__ __align__(16) int16_t sh16[];
+  __shared__ __align__(8) uint64_t tbar;
+  int64_t* sbuf = reinterpret_cast<int64_t*>(sh16);  // Geo (phase 0) / coefficient row (phase 1)
+  const uint32_t bytes = phase == 0 ? (uint32_t)sizeof(Geo) : (uint32_t)A * 64u;
+  if (bytes == 0) return;  // no accesses: nothing to move
+  if (threadIdx.x == 0) {
+    tma_bar_init(&tbar);
+    tma_load_1d(sbuf, phase == 0 ? (const void*)(slot + plan_geo_off()) : (const void*)(slot + plan_coef_off()),
+                bytes, &tbar);
+  }
+  __syncthreads();
+  tma_wait(&tbar, 0);
+  if (phase == 0) {
+    if (threadIdx.x == 0) {
+      tma_store_1d(geos + c, sbuf, bytes);
+      tma_store_commit_wait();
+    }
+    return;
+  }
+  // coefficients: the constant of an affine access moves with its field's base
+  for (int a = threadIdx.x; a < A; a += blockDim.x)
+    if (sbuf[a * 8 + 7] == kAffine) sbuf[a * 8] += dlt[T.acc_field[abase + a]];
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tma_store_1d(coefs + c * (int64_t)T.max_acc * 8, sbuf, bytes);
+    tma_store_commit_wait();
+  }
+#else
   if (phase == 0) {
     const int words = (int)(sizeof(Geo) / 4);
     const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(slot + plan_geo_off());
@@ -608,6 +680,7 @@ __global__ void __launch_bounds__(256) k_plan_follow(TplView T, const gvo_machin
     if (k == 0 && csrc[a * 8 + 7] == kAffine) v += dlt[T.acc_field[abase + a]];
     crow[i] = v;
   }
+#endif
   // class table: same classes, each class's sorted constants shifted by its field's delta
   const int64_t CS = ctab_stride(T.max_acc);
   const int64_t* tsrc = slot + plan_ctab_off(T.max_acc);
@@ -627,6 +700,19 @@ __global__ void __launch_bounds__(256) k_plan_follow(TplView T, const gvo_machin
   }
 }
 
+// dynamic shared memory of k_plan_follow: a follower that computes its own
+// plan (setup_one) or the TMA staging buffer (Geo / coefficient row)
+static size_t follow_smem(int max_acc) {
+  const size_t tma = std::max(sizeof(Geo), (size_t)max_acc * 64) + 16;
+  const size_t need = std::max(setup_smem(max_acc), tma);
+  static size_t attr = 0;
+  if (need > 48 * 1024 && need > attr) {
+    cudaFuncSetAttribute(k_plan_follow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
+    attr = need;
+  }
+  return need;
+}
+
 void launch_setup(const TplView& T, const gvo_machine* d_machines, const gvo_config* d_cfgs,
                   int64_t n, const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos, int64_t* d_ctabs,
                   cudaStream_t st, const int32_t* d_mclass, const PlanShare* share) {
@@ -639,11 +725,11 @@ void launch_setup(const TplView& T, const gvo_machine* d_machines, const gvo_con
   k_setup<<<(unsigned)n, 256, setup_smem(T.max_acc), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs, d_geos, d_ctabs,
                                                            PS);
   if (PS.src) {
-    k_plan_follow<<<(unsigned)n, 256, setup_smem(T.max_acc), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs, d_geos,
-                                                                   d_ctabs, PS, 0);
+    k_plan_follow<<<(unsigned)n, 256, follow_smem(T.max_acc), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs, d_geos,
+                                                                    d_ctabs, PS, 0);
     if (!PS.defer_rows)
-      k_plan_follow<<<(unsigned)n, 256, setup_smem(T.max_acc), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs, d_geos,
-                                                                     d_ctabs, PS, 1);
+      k_plan_follow<<<(unsigned)n, 256, follow_smem(T.max_acc), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs, d_geos,
+                                                                      d_ctabs, PS, 1);
   }
 }
 
@@ -651,8 +737,8 @@ void launch_plan_rows(const TplView& T, const gvo_machine* d_machines, const gvo
                       const gvo_sampling& smp, int64_t* d_coefs, Geo* d_geos, int64_t* d_ctabs, const PlanShare& PS,
                       cudaStream_t st) {
   if (n > 0 && PS.src)
-    k_plan_follow<<<(unsigned)n, 256, setup_smem(T.max_acc), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs, d_geos,
-                                                                   d_ctabs, PS, 1);
+    k_plan_follow<<<(unsigned)n, 256, follow_smem(T.max_acc), st>>>(T, d_machines, d_cfgs, n, smp, d_coefs, d_geos,
+                                                                    d_ctabs, PS, 1);
 }
 
 __global__ void k_classes_only(TplView T, const gvo_config* cfgs, int64_t n, const int64_t* coefs,
