@@ -218,7 +218,10 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n,
                      double* d_field_down, int64_t* d_l1_access,
                      int32_t l1_access_stride, void* stream);
 
-/* Same with host buffers: copies in, evaluates, copies out, synchronises. */
+/* Same with host buffers: copies in, evaluates, copies out, synchronises.
+ * When every output buffer is page-locked (cudaHostAlloc / pinned) and the
+ * call spans several batches, each batch's rows are copied to the host on a
+ * second stream while the next batches compute (gvo_sweep_host* likewise). */
 int gvo_eval_configs_host(gvo_ctx* ctx, const gvo_config* h_cfgs, int64_t n,
                           const gvo_sampling* sampling, int32_t F,
                           int64_t* h_counts, double* h_stats, double* h_records,

@@ -95,6 +95,19 @@ struct gvo_ctx {
   DBuf<int64_t> plan_cache, plan_src;
   DBuf<unsigned long long> plan_used;
   DBuf<uint8_t> plan_need;
+  // gvo_sweep_host_ex with pinned host outputs: each batch's finished rows
+  // are copied to the host on a second stream while later batches compute
+  struct PipeOut {
+    bool on = false;
+    int64_t* counts = nullptr;
+    double* stats = nullptr;
+    double* records = nullptr;
+    double* fd = nullptr;
+    int64_t* l1 = nullptr;
+    int32_t l1_stride = 0;
+  } pipe;
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> pipe_ev;
   // work lists of the set kernel (k_dedup.cu k_worklist), per batch
   bool worklist = true;
   int64_t handoff_min = 1024;  // batches from this size hand large block units to the CTA (GVO_HANDOFF_MIN)
@@ -353,6 +366,8 @@ void gvo_close(gvo_ctx* ctx) {
   ctx->s_gather.release();
   ctx->s_ull.release();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  for (cudaEvent_t e : ctx->pipe_ev) cudaEventDestroy(e);
   delete ctx;
 }
 
@@ -729,6 +744,30 @@ int gvo_eval_configs(gvo_ctx* ctx, const gvo_config* d_cfgs, int64_t n, const gv
                   d_field_down ? d_field_down + b0 * 4 * F : nullptr, st);
     tmark_end(ctx, 3, st, tb);
     CK(cudaGetLastError());
+    if (ctx->pipe.on) {  // this batch's rows are final: copy them out behind the next batches
+      const size_t bi = (size_t)(b0 / ctx->batch);
+      while (ctx->pipe_ev.size() <= bi) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->pipe_ev.push_back(e);
+      }
+      cudaStream_t cs = ctx->copy_stream;
+      CK(cudaEventRecord(ctx->pipe_ev[bi], st));
+      CK(cudaStreamWaitEvent(cs, ctx->pipe_ev[bi], 0));
+      const auto& po = ctx->pipe;
+      CK(cudaMemcpyAsync(po.counts + b0 * stride, cnt, (size_t)nb * stride * 8, cudaMemcpyDeviceToHost, cs));
+      CK(cudaMemcpyAsync(po.records + b0 * GVO_RECORD_LEN, d_records + b0 * GVO_RECORD_LEN,
+                         (size_t)nb * GVO_RECORD_LEN * 8, cudaMemcpyDeviceToHost, cs));
+      if (po.stats && d_stats)
+        CK(cudaMemcpyAsync(po.stats + b0 * GVO_STATS_LEN(F), d_stats + b0 * GVO_STATS_LEN(F),
+                           (size_t)nb * GVO_STATS_LEN(F) * 8, cudaMemcpyDeviceToHost, cs));
+      if (po.fd && d_field_down)
+        CK(cudaMemcpyAsync(po.fd + b0 * 4 * F, d_field_down + b0 * 4 * F, (size_t)nb * 4 * F * 8,
+                           cudaMemcpyDeviceToHost, cs));
+      if (po.l1 && d_l1_access)
+        CK(cudaMemcpyAsync(po.l1 + b0 * po.l1_stride * 3, d_l1_access + b0 * l1_stride * 3,
+                           (size_t)nb * l1_stride * 3 * 8, cudaMemcpyDeviceToHost, cs));
+    }
   }
   if (dd_stats) {
     unsigned long long h[2] = {0, 0};
@@ -755,6 +794,34 @@ int gvo_set_dedup(gvo_ctx* ctx, int enable) {
   return GVO_OK;
 }
 
+// Host-buffer entries: with page-locked outputs every batch's finished rows
+// are copied out on a second stream behind the next batches' kernels.
+// Returns 1 when the pipe is on (outputs then need no copy after the call).
+static int pipe_begin(gvo_ctx* ctx, int64_t n, int64_t* h_counts, double* h_stats, double* h_records,
+                      double* h_field_down, int64_t* h_l1_access, int32_t l1_stride) {
+  auto pinned = [](const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeHost;
+  };
+  const bool pipe = n > ctx->batch && pinned(h_counts) && pinned(h_records) && pinned(h_stats) &&
+                    pinned(h_field_down) && pinned(h_l1_access);
+  if (!pipe) return 0;
+  if (!ctx->copy_stream && cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  ctx->pipe.on = true;
+  ctx->pipe.counts = h_counts;
+  ctx->pipe.stats = h_stats;
+  ctx->pipe.records = h_records;
+  ctx->pipe.fd = h_field_down;
+  ctx->pipe.l1 = h_l1_access;
+  ctx->pipe.l1_stride = l1_stride;
+  return 1;
+}
+
 int gvo_eval_configs_host(gvo_ctx* ctx, const gvo_config* h_cfgs, int64_t n, const gvo_sampling* sampling,
                           int32_t F, int64_t* h_counts, double* h_stats, double* h_records,
                           double* h_field_down, int64_t* h_l1_access, int32_t l1_stride) {
@@ -772,16 +839,22 @@ int gvo_eval_configs_host(gvo_ctx* ctx, const gvo_config* h_cfgs, int64_t n, con
       (h_l1_access && !ctx->s_i64a.ensure(std::max<int64_t>(n * l1_stride * 3, 1))))
     return set_err(ctx, GVO_ERR_CUDA, "staging alloc failed%s");
   CK(cudaMemcpyAsync(ctx->s_cfgs.p, h_cfgs, n * sizeof(gvo_config), cudaMemcpyHostToDevice, st));
+  const int pipe = pipe_begin(ctx, n, h_counts, h_stats, h_records, h_field_down, h_l1_access, l1_stride);
   int rc = gvo_eval_configs(ctx, ctx->s_cfgs.p, n, sampling, F, ctx->s_counts.p,
                             h_stats ? ctx->s_stats.p : nullptr, ctx->s_records.p,
                             h_field_down ? ctx->s_fd.p : nullptr, h_l1_access ? ctx->s_i64a.p : nullptr,
                             l1_stride, st);
+  ctx->pipe.on = false;
+  if (pipe) CK(cudaStreamSynchronize(ctx->copy_stream));
   if (rc) return rc;
-  CK(cudaMemcpyAsync(h_counts, ctx->s_counts.p, n * stride * 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(h_records, ctx->s_records.p, n * GVO_RECORD_LEN * 8, cudaMemcpyDeviceToHost, st));
-  if (h_stats) CK(cudaMemcpyAsync(h_stats, ctx->s_stats.p, n * GVO_STATS_LEN(F) * 8, cudaMemcpyDeviceToHost, st));
-  if (h_field_down) CK(cudaMemcpyAsync(h_field_down, ctx->s_fd.p, n * 4 * F * 8, cudaMemcpyDeviceToHost, st));
-  if (h_l1_access) CK(cudaMemcpyAsync(h_l1_access, ctx->s_i64a.p, n * l1_stride * 3 * 8, cudaMemcpyDeviceToHost, st));
+  if (!pipe) {
+    CK(cudaMemcpyAsync(h_counts, ctx->s_counts.p, n * stride * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_records, ctx->s_records.p, n * GVO_RECORD_LEN * 8, cudaMemcpyDeviceToHost, st));
+    if (h_stats) CK(cudaMemcpyAsync(h_stats, ctx->s_stats.p, n * GVO_STATS_LEN(F) * 8, cudaMemcpyDeviceToHost, st));
+    if (h_field_down) CK(cudaMemcpyAsync(h_field_down, ctx->s_fd.p, n * 4 * F * 8, cudaMemcpyDeviceToHost, st));
+    if (h_l1_access)
+      CK(cudaMemcpyAsync(h_l1_access, ctx->s_i64a.p, n * l1_stride * 3 * 8, cudaMemcpyDeviceToHost, st));
+  }
   CK(cudaStreamSynchronize(st));
   return GVO_OK;
 }
@@ -804,19 +877,32 @@ int gvo_sweep_host_ex(gvo_ctx* ctx, const gvo_config* h_cfgs, int64_t n, const g
       !ctx->s_order.ensure(std::max<int64_t>(n, 1)))
     return set_err(ctx, GVO_ERR_CUDA, "staging alloc failed%s");
   CK(cudaMemcpyAsync(ctx->s_cfgs.p, h_cfgs, n * sizeof(gvo_config), cudaMemcpyHostToDevice, st));
+  // page-locked outputs: copy each batch out while the next ones compute
+  const int pipe = pipe_begin(ctx, n, h_counts, h_stats, h_records, h_field_down, h_l1_access, l1_stride);
   int rc = gvo_eval_configs(ctx, ctx->s_cfgs.p, n, sampling, F, ctx->s_counts.p, h_stats ? ctx->s_stats.p : nullptr,
                             ctx->s_records.p, h_field_down ? ctx->s_fd.p : nullptr,
                             h_l1_access ? ctx->s_i64a.p : nullptr, l1_stride, st);
-  if (rc) return rc;
+  ctx->pipe.on = false;
+  if (rc) {
+    if (pipe) cudaStreamSynchronize(ctx->copy_stream);
+    return rc;
+  }
   rc = gvo_rank(ctx, ctx->s_records.p, ctx->s_cfgs.p, n, ctx->s_order.p, st);
-  if (rc) return rc;
-  CK(cudaMemcpyAsync(h_counts, ctx->s_counts.p, n * stride * 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(h_records, ctx->s_records.p, n * GVO_RECORD_LEN * 8, cudaMemcpyDeviceToHost, st));
-  if (h_stats) CK(cudaMemcpyAsync(h_stats, ctx->s_stats.p, n * GVO_STATS_LEN(F) * 8, cudaMemcpyDeviceToHost, st));
-  if (h_field_down) CK(cudaMemcpyAsync(h_field_down, ctx->s_fd.p, n * 4 * F * 8, cudaMemcpyDeviceToHost, st));
-  if (h_l1_access) CK(cudaMemcpyAsync(h_l1_access, ctx->s_i64a.p, n * l1_stride * 3 * 8, cudaMemcpyDeviceToHost, st));
+  if (rc) {
+    if (pipe) cudaStreamSynchronize(ctx->copy_stream);
+    return rc;
+  }
+  if (!pipe) {
+    CK(cudaMemcpyAsync(h_counts, ctx->s_counts.p, n * stride * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_records, ctx->s_records.p, n * GVO_RECORD_LEN * 8, cudaMemcpyDeviceToHost, st));
+    if (h_stats) CK(cudaMemcpyAsync(h_stats, ctx->s_stats.p, n * GVO_STATS_LEN(F) * 8, cudaMemcpyDeviceToHost, st));
+    if (h_field_down) CK(cudaMemcpyAsync(h_field_down, ctx->s_fd.p, n * 4 * F * 8, cudaMemcpyDeviceToHost, st));
+    if (h_l1_access)
+      CK(cudaMemcpyAsync(h_l1_access, ctx->s_i64a.p, n * l1_stride * 3 * 8, cudaMemcpyDeviceToHost, st));
+  }
   CK(cudaMemcpyAsync(h_order, ctx->s_order.p, n * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (pipe) CK(cudaStreamSynchronize(ctx->copy_stream));
   return GVO_OK;
 }
 

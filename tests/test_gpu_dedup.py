@@ -106,3 +106,34 @@ def test_plan_sharing_with_failing_leaders():
         assert np.array_equal(on[k], off[k]), k
     for k in ("stats", "records"):
         assert np.array_equal(on[k].view(np.int64), off[k].view(np.int64)), k
+
+
+def test_pinned_sweep_host_pipelines_copies_identically():
+    """gvo_sweep_host_ex with page-locked outputs copies every batch to the
+    host behind the next batches' kernels (a second stream); every output
+    equals the pageable path's (one copy after the last batch)."""
+    import torch
+
+    sp = _slice()
+    ctx = _native.context()
+    cfgs = np.ascontiguousarray(sp.config_array(ctx))
+    assert len(cfgs) > 16384
+    ref = ctx.sweep_host(cfgs, 5, 2, 0)
+    F, S, Wn = ref["F"], ref["S"], ref["W"]
+    n, A = len(cfgs), ctx.max_accesses
+    pin = lambda shape, dt: torch.zeros(shape, dtype=dt, pin_memory=True).numpy()  # noqa: E731
+    counts = pin((n, _native.counts_stride(F, S, Wn)), torch.int64)
+    stats = pin((n, _native.stats_len(F)), torch.float64)
+    rec = pin((n, _native.RECORD_LEN), torch.float64)
+    fd = pin((n, 4, F), torch.float64)
+    l1 = pin((n, A, 3), torch.int64)
+    order = pin((n,), torch.int64)
+    smp = _native.Sampling(5, 2, 0, 7, 0)
+    ctx.check(_native.lib().gvo_sweep_host_ex(ctx.h, _native._ptr(cfgs), n, C.byref(smp), F, _native._ptr(counts),
+                                              _native._ptr(stats), _native._ptr(rec), _native._ptr(fd),
+                                              _native._ptr(l1), A, _native._ptr(order)))
+    assert np.array_equal(counts, ref["counts"])
+    assert np.array_equal(l1, ref["l1_access"])
+    assert np.array_equal(order, ref["order"])
+    for got, want in ((stats, ref["stats"]), (rec, ref["records"]), (fd, ref["field_down"])):
+        assert np.array_equal(got.view(np.int64), want.view(np.int64))
