@@ -59,6 +59,11 @@ constexpr int kSetsSmemBytes = kSetsCtasPerSm == 1 ? 222 * 1024 : kSetsCtasPerSm
 #else
 #define GVO_PH(...)
 #endif
+#if defined(GVO_PHASE_STATS) && GVO_PHASE_STATS && !(defined(GVO_BM_PROF) && GVO_BM_PROF)
+#define GVO_PHN(...) __VA_ARGS__  // slots 12..15 (segment counters, run-building split) unless GVO_BM_PROF
+#else
+#define GVO_PHN(...)
+#endif
 
 // out-of-line set-engine stages (own register allocation, fewer spills in
 // the monolithic kernel); GVO_HOT_NOINLINE=0 inlines them (A/B builds)
@@ -1654,21 +1659,34 @@ __device__ __forceinline__ void atom_counts(const uint32_t* bm, int64_t wp, int3
   }
 }
 
+// GVO_BM_PROF (with GVO_PHASE_STATS): bitmap-tier sub-phases into the
+// phase slots 12..15 (zeroing, element pass, big runs, measures) instead of
+// the segment counters (tools/phase_profile.py reads them under those names)
+#if defined(GVO_BM_PROF) && GVO_BM_PROF
+#define GVO_BMP(...) __VA_ARGS__
+#else
+#define GVO_BMP(...)
+#endif
 __device__ __noinline__ void bitmap_range(uint32_t* bm, const Run* druns, const int64_t* rcnt, const int64_t* rka, int nr,
                              int64_t N, int64_t a, int64_t b, int64_t kbase, int n_tags, const Granule& Gr,
                              const TplView& T, int abase, const int64_t* fbase, const int32_t bd[3],
                              const int64_t gd[3], int64_t tpb, UnitSh& U, int64_t* wmax, bool nonmono,
-                             uint32_t tag_mask, int* big_list, int big_cap) {
+                             uint32_t tag_mask, int* big_list, int big_cap GVO_BMP(, long long* php)) {
+  GVO_BMP(long long tb0 = clock64();)
   const int64_t wp = (b - a + 31) >> 5;
   // runs whose every interval covers >= kBigWords bitmap words (folded rows,
   // merged layers) are filled by the whole CTA after the element pass: one
   // thread per such interval would hold the CTA at the barrier
-  constexpr int64_t kBigWords = 32;
+#ifndef GVO_BIG_WORDS
+#define GVO_BIG_WORDS 256  // A/B on C4 / a C5 sample: 8, 16, 32 (r01), 64, 128, 256, 1024 -> 256 best (-3 %)
+#endif
+  constexpr int64_t kBigWords = GVO_BIG_WORDS;
   const uint64_t big_span = (uint64_t)(kBigWords * 32) * (uint64_t)Gr.g;
   __shared__ int n_big;
   if (threadIdx.x == 0) n_big = 0;
   for (int64_t i = threadIdx.x; i < (int64_t)n_tags * wp; i += kNT) bm[i] = 0u;
   __syncthreads();
+  GVO_BMP(if (threadIdx.x == 0) { const long long t = clock64(); php[12] += t - tb0; tb0 = t; })
   // monotone runs: elements rka[r] .. rka[r] + count, contiguous per thread.
   // Dim 0 is stepped incrementally; single-granule intervals that land in
   // the same bitmap word are OR-ed in a register before one atomicOr.
@@ -1734,6 +1752,7 @@ __device__ __noinline__ void bitmap_range(uint32_t* bm, const Run* druns, const 
     }
   }
   __syncthreads();
+  GVO_BMP(if (threadIdx.x == 0) { const long long t = clock64(); php[13] += t - tb0; tb0 = t; })
   // big runs: their (run, element) pairs dealt to warps, lanes over words
   {
     const int nb = min(n_big, big_cap / 2 - 1);
@@ -1808,6 +1827,7 @@ __device__ __noinline__ void bitmap_range(uint32_t* bm, const Run* druns, const 
     }
   }
   __syncthreads();
+  GVO_BMP(if (threadIdx.x == 0) { const long long t = clock64(); php[14] += t - tb0; tb0 = t; })
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // granule-resolution measures over <= 4 planes (wave-unit pieces): per word
   // the popcounts of the 2^T - 1 atoms (bits in exactly the planes of p), and
@@ -1848,6 +1868,7 @@ __device__ __noinline__ void bitmap_range(uint32_t* bm, const Run* druns, const 
       U.sub_val[threadIdx.x] = t;
     }
     __syncthreads();
+    GVO_BMP(if (threadIdx.x == 0) php[15] += clock64() - tb0;)
     return;
   }
   constexpr int kPcSub = 16, kPcTags = 8;
@@ -2895,7 +2916,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         }
       }
       // (b) lattices: one WARP per (source, box, coefficient class)
-      GVO_PH(__syncthreads(); if (threadIdx.x == 0) ph[14] += clock64() - t_start;)
+      GVO_PHN(__syncthreads(); if (threadIdx.x == 0) ph[14] += clock64() - t_start;)
       GVO_PH(const long long t_lat = clock64();)
       {
         const CTab ct{const_cast<int64_t*>(P.ctabs) + c * ctab_stride(P.T.max_acc), P.T.max_acc};
@@ -2958,12 +2979,12 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
             const bool segd = !P.seg_off && cover_segments(sink, L0, wpts, m, U.src_tag[s], Gr, seg,
                                                             !P.pat_off && (U.kind != 0 || P.mode != 0));
             if (!segd) cover_warp(sink, L0, wpts, m, U.src_tag[s], Gr);
-            GVO_PH(if (lane == 0) atomicAdd((unsigned long long*)&ph[segd ? 12 : 13], 1ull);)
+            GVO_PHN(if (lane == 0) atomicAdd((unsigned long long*)&ph[segd ? 12 : 13], 1ull);)
           }
         }
       }
       __syncthreads();
-      GVO_PH(if (threadIdx.x == 0) ph[15] += clock64() - t_lat;)
+      GVO_PHN(if (threadIdx.x == 0) ph[15] += clock64() - t_lat;)
 
     if (threadIdx.x == 0) { t_runs_sh = clock64(); GVO_PH(ph[3] += t_runs_sh - t_start;) }
     // ---------------- offsets of runs, element count
@@ -3308,7 +3329,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         bitmap_range(reinterpret_cast<uint32_t*>(ebuf), druns, rcnt, rka, nr, N, a, b, kbase,
                      max(1, __popc(s_rtags & tag_mask)), Gr, P.T, abase,
                      fbase, bd, gd, tpb, U, wmax, s_nonmono != 0, s_rtags & tag_mask, reinterpret_cast<int*>(hist),
-                     kNW * 256);
+                     kNW * 256 GVO_BMP(, ph));
         if (threadIdx.x < U.n_sub) atomicAdd(&hdr->acc[threadIdx.x], (unsigned long long)U.sub_val[threadIdx.x]);
         GVO_PH(if (threadIdx.x == 0) ph[6] += clock64() - t_r1;)
       } else if (N > P.elem_cap || has_pat) {

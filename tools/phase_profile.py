@@ -41,6 +41,8 @@ print(f"{part} configs {c0}..{c0 + len(sp)}: CTAs {len(ph)}; phase Gcycles (sum 
       {k: round(float(v), 3) for k, v in zip(names, tot)})
 print("ranges", int(ph[:, 8].sum()), "bitmap", int(ph[:, 9].sum()), "sum N", int(ph[:, 10].sum()), "sum nr",
       int(ph[:, 11].sum()), "seg ok", int(ph[:, 12].sum()), "seg no", int(ph[:, 13].sum()))
+print("slots 12..15 Gcycles (bmprof build: bitmap zero/elements/big runs/measures)",
+      np.round(ph[:, 12:16].sum(0) / 1e9, 3).tolist())
 busy = ph[:, 1:8].sum(1) / 1e3
 print("per-CTA fetch-wait kcycles p50/max", np.percentile(ph[:, 0] / 1e3, [50, 100]).round(0),
       "busy kcycles p10/p50/p90/max", np.percentile(busy, [10, 50, 90, 100]).round(0))
