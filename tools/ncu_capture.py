@@ -46,7 +46,8 @@ FULL_PICK = {
     "duration": "gpu__time_duration.sum",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-         "msecond": 1e-3, "second": 1.0, "inst": 1, "": 1, "%": 1, "cycle": 1}
+         "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0,
+         "inst": 1, "": 1, "%": 1, "cycle": 1}
 
 
 def _rows(text):
