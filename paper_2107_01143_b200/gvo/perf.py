@@ -183,7 +183,7 @@ class SweepPlan:
                 break
             block[i], grid[i], wpt[i], flops[i] = launch.block_dim, launch.grid_dim, launch.work_per_thread, fl
         idx = np.flatnonzero(keep)
-        self.configs = [configs[i] for i in idx]
+        self.configs = configs if len(idx) == n else [configs[i] for i in idx.tolist()]
         self.block, self.grid, self.wpt, self.flops = block[idx], grid[idx], wpt[idx], flops[idx]
         # one template per key (built from its first configuration), ids registered once
         self.templates: list = []
@@ -206,7 +206,8 @@ class SweepPlan:
                             _TPL_CACHE.clear()
                         _TPL_CACHE[(family, tkey[i])] = (k, ctx, tid)
             self.tpl[j] = t
-        self.fold_rank = np.array([_engine.FOLD_RANK[c.folding] for c in self.configs], dtype=np.int32)
+        fr = _engine.FOLD_RANK
+        self.fold_rank = np.array([fr[c.folding] for c in self.configs], dtype=np.int32)
 
     def __len__(self) -> int:
         return len(self.configs)
