@@ -1993,6 +1993,9 @@ struct SetsArgs {
 // own shared-memory slice, bitonic-sorts them in place (the sweep needs key
 // order only, not stability) and sweeps.  Units that do not fit fall back to
 // the CTA path.
+#ifndef GVO_TASK_DYN
+#define GVO_TASK_DYN 1
+#endif
 #ifndef GVO_BLOCK_POOL
 #define GVO_BLOCK_POOL 0  // A/B: 1 = warp-scheduled block-unit pool (C5 stencil part 330 vs 312 ms: rejected)
 #endif
@@ -2932,6 +2935,7 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
         // them evenly (empty store sources and absent boxes are skipped);
         // the element buffer is free while runs are built
         __shared__ int n_tasks_sh;
+        __shared__ int task_next;  // GVO_TASK_DYN: next lattice task
         int* tlist = reinterpret_cast<int*>(ebuf);
         const int tcap = (int)min((int64_t)1 << 20, sm_elems * 4);
         if (threadIdx.x == 0) {
@@ -2948,12 +2952,21 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
               }
           }
           n_tasks_sh = nt;
+          task_next = kNW;
         }
         __syncthreads();
         const int n_tasks = n_tasks_sh;
         const bool listed = n_tasks >= 0 && ncl < 65536;
         const int n_iter = listed ? n_tasks : U.n_src * 5 * ncl;
+#if GVO_TASK_DYN
+        // tasks taken from a shared counter (their costs differ by an order of
+        // magnitude: a 25-point load class vs a one-point store class)
+        for (int task = wid;;) {
+          if (task >= n_iter) break;
+#else
         for (int task = wid; task < n_iter; task += kNW) {
+#endif
+         do {
           int s, bi, ci;
           if (listed) {
             const int t = tlist[task];
@@ -2963,9 +2976,9 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
           }
           const int slot = slot0 + U.src_kind[s];
           const int64_t cl0 = ct.slot_first()[slot];
-          if (ci >= ct.slot_first()[slot + 1] - cl0) continue;
+          if (ci >= ct.slot_first()[slot + 1] - cl0) break;
           Box box;
-          if (!run_box_at(U.src_start[s], U.src_count[s], gd, bi, &box)) continue;
+          if (!run_box_at(U.src_start[s], U.src_count[s], gd, bi, &box)) break;
           const int64_t cls = cl0 + ci;
           const int64_t* ca = crow + ct.rep()[cls] * 8;
           const WLat L0 = box_lattice(ca, bd, box, Gr);
@@ -2981,6 +2994,12 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
             if (!segd) cover_warp(sink, L0, wpts, m, U.src_tag[s], Gr);
             GVO_PHN(if (lane == 0) atomicAdd((unsigned long long*)&ph[segd ? 12 : 13], 1ull);)
           }
+         } while (0);
+#if GVO_TASK_DYN
+          int nxt = 0;
+          if (lane == 0) nxt = atomicAdd(&task_next, 1);
+          task = __shfl_sync(0xffffffffu, nxt, 0);
+#endif
         }
       }
       __syncthreads();
