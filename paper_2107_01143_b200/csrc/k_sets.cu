@@ -75,6 +75,40 @@ constexpr int kSetsSmemBytes = kSetsCtasPerSm == 1 ? 222 * 1024 : kSetsCtasPerSm
 #else
 #define GVO_NOINL
 #endif
+// Instruction footprint: the kernel is one ~1.5 MB SASS image and
+// instruction-fetch stalls were 18 % of its warp samples (ncu, C5).  Device
+// functions inlined at several call sites are kept as one out-of-line copy
+// where that measured faster; GVO_OUTLINE is a bit mask (A/B builds):
+//   1 wl_emit_lattice (3 call sites in cover_warp; C5 sample -11 %),
+//   2 box_lattice, 4 wl_emit_normalized, 8 run_interval, 16 wl_normalize
+#ifndef GVO_OUTLINE
+#define GVO_OUTLINE 1
+#endif
+#if GVO_OUTLINE & 1
+#define GVO_OL_EMIT __noinline__
+#else
+#define GVO_OL_EMIT __forceinline__
+#endif
+#if GVO_OUTLINE & 2
+#define GVO_OL_BOX __noinline__
+#else
+#define GVO_OL_BOX inline
+#endif
+#if GVO_OUTLINE & 4
+#define GVO_OL_EMITN __noinline__
+#else
+#define GVO_OL_EMITN __forceinline__
+#endif
+#if GVO_OUTLINE & 8
+#define GVO_OL_RIV __noinline__
+#else
+#define GVO_OL_RIV __forceinline__
+#endif
+#if GVO_OUTLINE & 16
+#define GVO_OL_NORM __noinline__
+#else
+#define GVO_OL_NORM __forceinline__
+#endif
 
 // threads per CTA.  2 CTAs/SM: 320 threads (96 registers; A/B on C2:
 // 320 > 384 > 256 > 512, the 64-register build spills its stack to DRAM);
@@ -161,7 +195,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // stride, st_j % st_i == 0 && st_j / st_i <= ex_i), then fold the leading
 // dims whose point gaps stay <= g into the granule-contiguous span.
 // Warp-cooperative; dims with ex <= 1 or st == 0 are dropped.
-__device__ __forceinline__ void wl_normalize(WLat& L, int64_t g) {
+__device__ GVO_OL_NORM void wl_normalize(WLat& L, int64_t g) {
   const int lane = threadIdx.x & 31;
   const bool keep = lane < L.nd && L.ex > 1 && L.st != 0;
   const unsigned kmask = __ballot_sync(kFull, keep);
@@ -238,7 +272,7 @@ struct RunSink {
 // differ in their base: one run per active lane (`act`, this lane's base
 // `b`).  Warp-cooperative: one slot reservation, the dims written by the
 // lanes that hold them.
-__device__ __forceinline__ void wl_emit_normalized(const RunSink& S, const WLat& L, int64_t b, bool act, int tag,
+__device__ GVO_OL_EMITN void wl_emit_normalized(const RunSink& S, const WLat& L, int64_t b, bool act, int tag,
                                                 const Granule& G) {
   const int lane = threadIdx.x & 31;
   int64_t count = 1;
@@ -312,7 +346,7 @@ __device__ __forceinline__ void wl_emit_normalized(const RunSink& S, const WLat&
 // instead of scanning.  Splitting is bounded (<= 64 sub-lattices, emitted
 // by the lanes in parallel); beyond that the lattice is emitted as one
 // non-monotone run.  Warp-cooperative.
-__device__ __forceinline__ void wl_emit_lattice(const RunSink& S, WLat L, int tag, const Granule& G) {
+__device__ GVO_OL_EMIT void wl_emit_lattice(const RunSink& S, WLat L, int tag, const Granule& G) {
   const int lane = threadIdx.x & 31;
   wl_normalize(L, G.g);
   unsigned smask = 0;
@@ -1141,7 +1175,7 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const WLat& L0, co
 
 // lattice of one coefficient vector over one block box, translation 0
 // (warp-cooperative: lane k < 6 holds coordinate k = tid x/y/z, bid x/y/z)
-__device__ inline WLat box_lattice(const int64_t* c, const int32_t bd[3], const Box& b, const Granule& G) {
+__device__ GVO_OL_BOX WLat box_lattice(const int64_t* c, const int32_t bd[3], const Box& b, const Granule& G) {
   const int lane = threadIdx.x & 31;
   int64_t ext = 1, co = 0;
   uint64_t contrib = 0;
@@ -1164,29 +1198,55 @@ __device__ inline WLat box_lattice(const int64_t* c, const int32_t bd[3], const 
 
 
 // ------------------------------------------------------------------ decode
-// tuple k of a lattice run -> base address (dim 0 fastest)
-__device__ __forceinline__ uint64_t run_base(const Run& r, int64_t k) {
+// tuple k of a lattice run -> base address (dim 0 fastest).  The 64-bit
+// decode (k >= 2^31, rare) is kept out of line: its divisions would
+// otherwise be inlined at every call site (~1.3 k instructions each, the
+// largest share of the kernel's 1.5 MB of code and of its instruction-fetch
+// stalls).
+__device__ __noinline__ uint64_t run_base_wide(const Run& r, int64_t k) {
   uint64_t b = (uint64_t)r.base;
-  if (k < (int64_t(1) << 31)) {
-    uint32_t k32 = (uint32_t)k;
-    for (int d = 0; d < r.nd; ++d) {
-      const uint32_t ex = (uint32_t)r.ext[d];
-      const uint32_t q = k32 / ex;
-      b += (uint64_t)r.stride[d] * (uint64_t)(k32 - q * ex);
-      k32 = q;
-    }
-  } else {
-    for (int d = 0; d < r.nd; ++d) {
-      const int64_t idx = k % r.ext[d];
-      k /= r.ext[d];
-      b += (uint64_t)r.stride[d] * (uint64_t)idx;
-    }
+  for (int d = 0; d < r.nd; ++d) {
+    const int64_t idx = k % r.ext[d];
+    k /= r.ext[d];
+    b += (uint64_t)r.stride[d] * (uint64_t)idx;
   }
   return b;
 }
 
+__device__ __forceinline__ uint64_t run_base(const Run& r, int64_t k) {
+  if (k >= (int64_t(1) << 31)) return run_base_wide(r, k);
+  uint64_t b = (uint64_t)r.base;
+  uint32_t k32 = (uint32_t)k;
+  for (int d = 0; d < r.nd; ++d) {
+    const uint32_t ex = (uint32_t)r.ext[d];
+    const uint32_t q = k32 / ex;
+    b += (uint64_t)r.stride[d] * (uint64_t)(k32 - q * ex);
+    k32 = q;
+  }
+  return b;
+}
+
+// element k of a points run (non-affine access: one bytecode evaluation per
+// (block, thread)) -> its granule; out of line like run_base_wide (cold in
+// affine workloads, the interpreter is large)
+__device__ __noinline__ int64_t run_point_granule(const Run& r, int64_t k, const Granule& Gr, const TplView& T,
+                                                  int abase, const int64_t* fbase, const int32_t* bd,
+                                                  const int64_t* gd, int64_t tpb) {
+  const int64_t blk = r.run_start + k / tpb;
+  const int64_t th = k % tpb;
+  int64_t crd[6];
+  crd[0] = th % bd[0];
+  crd[1] = (th / bd[0]) % bd[1];
+  crd[2] = th / ((int64_t)bd[0] * bd[1]);
+  crd[3] = blk % gd[0];
+  crd[4] = (blk / gd[0]) % gd[1];
+  crd[5] = blk / (gd[0] * gd[1]);
+  const int ga = abase + r.access;
+  return Gr.of(eval_point(T.code + T.code_off[ga], T.code_len[ga], crd, bd, fbase));
+}
+
 // element k of any run -> absolute granule interval [glo, ghi]
-__device__ __forceinline__ void run_interval(const Run& r, int64_t k, const Granule& Gr, const TplView& T, int abase,
+__device__ GVO_OL_RIV void run_interval(const Run& r, int64_t k, const Granule& Gr, const TplView& T, int abase,
                                              const int64_t* fbase, const int32_t bd[3], const int64_t gd[3],
                                              int64_t tpb, int64_t* glo, int64_t* ghi) {
   if (r.kind == 0) {
@@ -1203,17 +1263,7 @@ __device__ __forceinline__ void run_interval(const Run& r, int64_t k, const Gran
     *glo = lo;
     *ghi = hi;
   } else {
-    const int64_t blk = r.run_start + k / tpb;
-    const int64_t th = k % tpb;
-    int64_t crd[6];
-    crd[0] = th % bd[0];
-    crd[1] = (th / bd[0]) % bd[1];
-    crd[2] = th / ((int64_t)bd[0] * bd[1]);
-    crd[3] = blk % gd[0];
-    crd[4] = (blk / gd[0]) % gd[1];
-    crd[5] = blk / (gd[0] * gd[1]);
-    const int ga = abase + r.access;
-    *glo = *ghi = Gr.of(eval_point(T.code + T.code_off[ga], T.code_len[ga], crd, bd, fbase));
+    *glo = *ghi = run_point_granule(r, k, Gr, T, abase, fbase, bd, gd, tpb);
   }
 }
 
