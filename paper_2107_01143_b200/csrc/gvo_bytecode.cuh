@@ -11,6 +11,12 @@
 //                      failing when a node leaves int64 (expr.value_bounds,
 //                      expr.py:127-168, the AddressOverflowError guard).
 #pragma once
+// GVO_OUTLINE bit 64 (k_sets.cu): evaluator and guard as one out-of-line copy
+#if defined(GVO_OUTLINE) && (GVO_OUTLINE & 64)
+#define GVO_BC_ATTR inline __noinline__
+#else
+#define GVO_BC_ATTR inline
+#endif
 #include "gvo_common.cuh"
 
 namespace gvo {
@@ -85,7 +91,7 @@ __device__ inline int affine_extract(const gvo_insn* code, int len, const int32_
 }
 
 // Wrapping int64 evaluation; exact whenever bounds_check passed.
-__device__ inline int64_t eval_point(const gvo_insn* code, int len, const int64_t coord[6],
+__device__ GVO_BC_ATTR int64_t eval_point(const gvo_insn* code, int len, const int64_t coord[6],
                                      const int32_t bd[3], const int64_t* field_base) {
   int64_t st[kStack];
   int sp = 0;
@@ -117,7 +123,7 @@ __device__ inline int64_t eval_point(const gvo_insn* code, int len, const int64_
 // instruction index of the first failing node.  lo/hi receive the root
 // interval on success.
 // *mag (optional) receives the largest |bound| of any BinOp node.
-__device__ inline int bounds_check(const gvo_insn* code, int len, const int64_t clo[6],
+__device__ GVO_BC_ATTR int bounds_check(const gvo_insn* code, int len, const int64_t clo[6],
                                    const int64_t chi[6], const int32_t bd[3],
                                    const int64_t* field_base, int64_t* root_lo,
                                    int64_t* root_hi, uint64_t* mag = nullptr) {

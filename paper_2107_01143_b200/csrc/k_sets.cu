@@ -81,8 +81,11 @@ constexpr int kSetsSmemBytes = kSetsCtasPerSm == 1 ? 222 * 1024 : kSetsCtasPerSm
 // where that measured faster; GVO_OUTLINE is a bit mask (A/B builds):
 //   1 wl_emit_lattice (3 call sites in cover_warp; C5 sample -11 %),
 //   2 box_lattice, 4 wl_emit_normalized, 8 run_interval, 16 wl_normalize
+//   (each within +-2 % or slower), 32 run_base's dimension loop not unrolled
+//   (-2.6 %), 64 bytecode evaluator / interval guard out of line
+//   (gvo_bytecode.cuh; +0.5 %), 128 wl_normalize's loops not unrolled (-2.4 %)
 #ifndef GVO_OUTLINE
-#define GVO_OUTLINE 1
+#define GVO_OUTLINE 161
 #endif
 #if GVO_OUTLINE & 1
 #define GVO_OL_EMIT __noinline__
@@ -201,12 +204,18 @@ __device__ GVO_OL_NORM void wl_normalize(WLat& L, int64_t g) {
   const unsigned kmask = __ballot_sync(kFull, keep);
   // rank among kept dims by (stride, dim)
   int r = 0;
+#if GVO_OUTLINE & 128
+#pragma unroll 1
+#endif
   for (int j = 0; j < L.nd; ++j) {
     const uint64_t sj = __shfl_sync(kFull, L.st, j);
     r += ((kmask >> j) & 1u) && (sj < L.st || (sj == L.st && j < lane));
   }
   uint64_t s2 = 0;
   int64_t e2 = 1;
+#if GVO_OUTLINE & 128
+#pragma unroll 1
+#endif
   for (int j = 0; j < L.nd; ++j) {
     const int rj = __shfl_sync(kFull, r, j);
     const uint64_t sj = __shfl_sync(kFull, L.st, j);
@@ -217,6 +226,9 @@ __device__ GVO_OL_NORM void wl_normalize(WLat& L, int64_t g) {
   uint64_t so = 0;
   int64_t eo = 1;
   int o = 0;
+#if GVO_OUTLINE & 128
+#pragma unroll 1
+#endif
   for (int i = 0; i < m; ++i) {
     const uint64_t si = __shfl_sync(kFull, s2, i);
     const int64_t ei = __shfl_sync(kFull, e2, i);
@@ -1217,6 +1229,9 @@ __device__ __forceinline__ uint64_t run_base(const Run& r, int64_t k) {
   if (k >= (int64_t(1) << 31)) return run_base_wide(r, k);
   uint64_t b = (uint64_t)r.base;
   uint32_t k32 = (uint32_t)k;
+#if GVO_OUTLINE & 32
+#pragma unroll 1
+#endif
   for (int d = 0; d < r.nd; ++d) {
     const uint32_t ex = (uint32_t)r.ext[d];
     const uint32_t q = k32 / ex;
