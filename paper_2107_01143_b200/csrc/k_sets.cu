@@ -84,8 +84,10 @@ constexpr int kSetsSmemBytes = kSetsCtasPerSm == 1 ? 222 * 1024 : kSetsCtasPerSm
 //   (each within +-2 % or slower), 32 run_base's dimension loop not unrolled
 //   (-2.6 %), 64 bytecode evaluator / interval guard out of line
 //   (gvo_bytecode.cuh; +0.5 %), 128 wl_normalize's loops not unrolled (-2.4 %)
+//   256 the other WLat emission loops not unrolled (-1.5 %), 512
+//   cover_segments' loops (neutral)
 #ifndef GVO_OUTLINE
-#define GVO_OUTLINE 161
+#define GVO_OUTLINE 417
 #endif
 #if GVO_OUTLINE & 1
 #define GVO_OL_EMIT __noinline__
@@ -292,6 +294,9 @@ __device__ GVO_OL_EMITN void wl_emit_normalized(const RunSink& S, const WLat& L,
   bool over = false;
   bool mono = true;
   unsigned __int128 reach = (unsigned __int128)L.span;
+#if GVO_OUTLINE & 256
+  #pragma unroll 1
+#endif
   for (int d = 0; d < L.nd; ++d) {
     const uint64_t sd = __shfl_sync(kFull, L.st, d);
     const int64_t ed = __shfl_sync(kFull, L.ex, d);
@@ -365,6 +370,9 @@ __device__ GVO_OL_EMIT void wl_emit_lattice(const RunSink& S, WLat L, int tag, c
   int64_t combos = 1;
   {
     unsigned __int128 reach = (unsigned __int128)L.span;
+#if GVO_OUTLINE & 256
+    #pragma unroll 1
+#endif
     for (int d = 0; d < L.nd; ++d) {
       const uint64_t sd = __shfl_sync(kFull, L.st, d);
       const int64_t ed = __shfl_sync(kFull, L.ex, d);
@@ -389,6 +397,9 @@ __device__ GVO_OL_EMIT void wl_emit_lattice(const RunSink& S, WLat L, int tag, c
   K.base = L.base;
   K.st = 0;
   K.ex = 1;
+#if GVO_OUTLINE & 256
+  #pragma unroll 1
+#endif
   for (int d = 0; d < L.nd; ++d) {
     const uint64_t sd = __shfl_sync(kFull, L.st, d);
     const int64_t ed = __shfl_sync(kFull, L.ex, d);
@@ -399,6 +410,9 @@ __device__ GVO_OL_EMIT void wl_emit_lattice(const RunSink& S, WLat L, int tag, c
     const int m = m0 + lane;
     int64_t r = m;
     uint64_t b = (uint64_t)L.base;
+#if GVO_OUTLINE & 256
+    #pragma unroll 1
+#endif
     for (int d = 0; d < L.nd; ++d) {
       const uint64_t sd = __shfl_sync(kFull, L.st, d);
       const int64_t ed = __shfl_sync(kFull, L.ex, d);
@@ -932,6 +946,9 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const WLat& L0, co
   if (!__all_sync(0xffffffffu, cont)) return false;
   // 3. breakpoints per dimension: distinct offsets D, merged with D + ex
   int64_t nbox = 1;
+#if GVO_OUTLINE & 512
+  #pragma unroll 1
+#endif
   for (int d = 0; d < nd; ++d) {
     const int32_t ex = (int32_t)sc->l0ex[d];
     int32_t v[2];
@@ -1016,6 +1033,9 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const WLat& L0, co
   // 4. per-dimension segment masks over sorted positions (lane holds
   // segments lane and lane + 32)
   bool fly = false;  // a dimension with > 64 segments: masks computed per box
+#if GVO_OUTLINE & 512
+  #pragma unroll 1
+#endif
   for (int d = 0; d < nd; ++d) fly |= sc->nb[d] - 1 > 64;
   uint64_t segm[kSegDims][2];
 #pragma unroll
@@ -1036,6 +1056,9 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const WLat& L0, co
   }
   // 5. plan: elements and runs of the segment cover vs. cover_warp's clusters
   double vol0 = 1.0;
+#if GVO_OUTLINE & 512
+  #pragma unroll 1
+#endif
   for (int d = 0; d < nd; ++d) vol0 *= (double)sc->l0ex[d];
   double seg_el = 0.0;
   int64_t seg_runs = 0;
@@ -1061,6 +1084,9 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const WLat& L0, co
       M = 0;
       for (int r2 = 0; r2 < n; ++r2) {
         bool in = true;
+#if GVO_OUTLINE & 512
+        #pragma unroll 1
+#endif
         for (int d = 0; d < nd && in; ++d) {
           const int32_t k = sc->kv[d][sc->ord[r2]];
           in = k <= sc->bpf[sc->boff[d] + sd[d]] && sc->bpf[sc->boff[d] + sd[d] + 1] <= k + (int32_t)sc->l0ex[d];
@@ -1070,6 +1096,9 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const WLat& L0, co
     }
     if (b >= nbox || !M) continue;
     double vol = 1.0;
+#if GVO_OUTLINE & 512
+    #pragma unroll 1
+#endif
     for (int d = 0; d < nd; ++d) vol *= (double)(sc->bpf[sc->boff[d] + sd[d] + 1] - sc->bpf[sc->boff[d] + sd[d]]);
     const double len0 = (double)(sc->bpf[sc->boff[0] + sd[0] + 1] - sc->bpf[sc->boff[0] + sd[0]]);
     uint64_t mm = M;
@@ -1120,6 +1149,9 @@ __device__ __noinline__ bool cover_segments(const RunSink& S, const WLat& L0, co
       M = 0;
       for (int r2 = 0; r2 < n; ++r2) {
         bool in = true;
+#if GVO_OUTLINE & 512
+        #pragma unroll 1
+#endif
         for (int d = 0; d < nd && in; ++d) {
           const int32_t k = sc->kv[d][sc->ord[r2]];
           in = k <= sc->bpf[sc->boff[d] + sd[d]] && sc->bpf[sc->boff[d] + sd[d] + 1] <= k + (int32_t)sc->l0ex[d];
@@ -3164,6 +3196,9 @@ __global__ void __launch_bounds__(kNT, kSetsCtasPerSm) k_sets(SetsArgs P) {
             int64_t lo = INT64_MIN, hi = INT64_MAX;  // points runs: unknown extent
             if (rr.kind != 1) {
               uint64_t ext = rr.span;
+#if GVO_OUTLINE & 256
+              #pragma unroll 1
+#endif
               for (int d = 0; d < rr.nd; ++d) ext += (uint64_t)rr.stride[d] * (uint64_t)(rr.ext[d] - 1);
               lo = Gr.of(rr.base) - U.key_lo;
               hi = Gr.of((int64_t)((uint64_t)rr.base + ext)) - U.key_lo;
