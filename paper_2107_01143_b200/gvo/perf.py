@@ -132,8 +132,21 @@ class SweepPlan:
         grid = np.zeros((n, 3), dtype=np.int64)
         wpt = np.ones(n, dtype=np.int64)
         flops = np.zeros(n, dtype=np.int64)
-        tkey = [None] * n
+        # template key of each configuration as an id into key_list (keys are
+        # large tuples: hashed once per distinct folding, not per config)
+        key_list: list = []
+        key_ix: dict = {}
+
+        def key_id(k) -> int:
+            j = key_ix.get(k)
+            if j is None:
+                j = key_ix[k] = len(key_list)
+                key_list.append(k)
+            return j
+
+        tk = np.full(n, -1, dtype=np.int64)
         fast = np.zeros(n, dtype=bool)
+        folds = None
         if family.kind in ("stencil", "lbm") and len(tuple(family.grid)) == 3:
             try:
                 b = np.array([c.block_dim for c in configs], dtype=np.int64)
@@ -141,9 +154,17 @@ class SweepPlan:
             except (TypeError, ValueError):
                 ok_shape = False
             if ok_shape:
+                # foldings as codes into their distinct values (a handful per sweep)
                 folds = [c.folding for c in configs]
-                ff = np.array([_FOLD_FACTORS.get(f, (0, 0, 0)) if isinstance(f, str) else (0, 0, 0)
-                               for f in folds], dtype=np.int64)
+                try:
+                    ufolds = [f for f in dict.fromkeys(folds) if isinstance(f, str)]
+                    ucode = {f: i for i, f in enumerate(ufolds)}
+                    fcode = np.array([ucode.get(f, -1) for f in folds], dtype=np.int64)
+                except TypeError:  # unhashable foldings: none of them is valid
+                    ufolds = []
+                    fcode = np.full(n, -1, dtype=np.int64)
+                uff = np.array([_FOLD_FACTORS.get(f, (0, 0, 0)) for f in ufolds] + [(0, 0, 0)], dtype=np.int64)
+                ff = uff[fcode]
                 g = np.array([int(v) for v in family.grid], dtype=np.int64)
                 eff = b * ff
                 ok = (ff > 0).all(axis=1) & (b >= 1).all(axis=1) & (g >= 1).all()
@@ -159,21 +180,18 @@ class SweepPlan:
                 grid[ok] = g[None, :] // np.where(eff[ok] > 0, eff[ok], 1)
                 wpt[ok] = ff[ok].prod(axis=1)
                 flops[ok] = fl
-                # stencil / lbm template keys depend on the folding only
-                kf: dict = {}
-                for i in np.flatnonzero(ok).tolist():
-                    f = folds[i]
-                    k = kf.get(f)
-                    if k is None:
-                        k = kf[f] = family.template_key(configs[i])
-                    tkey[i] = k
+                # stencil / lbm template keys depend on the folding only: one
+                # key per distinct folding, from its first valid configuration
+                for u in np.unique(fcode[ok]).tolist():
+                    rows = ok & (fcode == u)
+                    tk[rows] = key_id(family.template_key(configs[int(np.argmax(rows))]))
         self.build_error = None  # (index, exception) of the first invalid config (skip_invalid=False)
         keep = np.ones(n, dtype=bool)
         for i in np.flatnonzero(~fast):
             cfg = configs[i]
             try:
                 launch, fl = family.launch_of(cfg)
-                tkey[i] = family.template_key(cfg)
+                tk[i] = key_id(family.template_key(cfg))
             except ValueError as exc:
                 keep[i] = False
                 if skip_invalid:
@@ -187,27 +205,30 @@ class SweepPlan:
         self.block, self.grid, self.wpt, self.flops = block[idx], grid[idx], wpt[idx], flops[idx]
         # one template per key (built from its first configuration), ids registered once
         self.templates: list = []
-        tix: dict = {}
-        self.tpl = np.zeros(len(idx), dtype=np.int32)
+        ukid, first, kid = np.unique(tk[idx], return_index=True, return_inverse=True)
         cacheable = family.kind in ("stencil", "lbm")
-        for j, i in enumerate(idx):
-            t = tix.get(tkey[i])
-            if t is None:
-                t = tix[tkey[i]] = len(self.templates)
-                hit = _TPL_CACHE.get((family, tkey[i])) if cacheable else None
-                if hit is not None and hit[1] is ctx:
-                    self.templates.append((hit[0], hit[2]))
-                else:
-                    k = family.build(configs[i])
-                    tid = ctx.template_id(k.fields, k.accesses)
-                    self.templates.append((k, tid))
-                    if cacheable:
-                        if len(_TPL_CACHE) >= 4096:
-                            _TPL_CACHE.clear()
-                        _TPL_CACHE[(family, tkey[i])] = (k, ctx, tid)
-            self.tpl[j] = t
+        for u, j in zip(ukid.tolist(), first.tolist()):
+            key, i = key_list[u], int(idx[j])
+            hit = _TPL_CACHE.get((family, key)) if cacheable else None
+            if hit is not None and hit[1] is ctx:
+                self.templates.append((hit[0], hit[2]))
+            else:
+                k = family.build(configs[i])
+                tid = ctx.template_id(k.fields, k.accesses)
+                self.templates.append((k, tid))
+                if cacheable:
+                    if len(_TPL_CACHE) >= 4096:
+                        _TPL_CACHE.clear()
+                    _TPL_CACHE[(family, key)] = (k, ctx, tid)
+        self.tpl = kid.astype(np.int32).reshape(-1)
         fr = _engine.FOLD_RANK
-        self.fold_rank = np.array([fr[c.folding] for c in self.configs], dtype=np.int32)
+        if folds is not None and all(isinstance(f, str) for f in ufolds):
+            ufr = np.array([fr.get(f, -1) for f in ufolds] + [-1], dtype=np.int32)
+            self.fold_rank = ufr[fcode[idx]]
+            if (self.fold_rank < 0).any():  # a folding the rank table lacks: the reference's KeyError
+                self.fold_rank = np.array([fr[c.folding] for c in self.configs], dtype=np.int32)
+        else:
+            self.fold_rank = np.array([fr[c.folding] for c in self.configs], dtype=np.int32)
 
     def __len__(self) -> int:
         return len(self.configs)
