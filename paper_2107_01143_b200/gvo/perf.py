@@ -14,6 +14,9 @@ from dataclasses import dataclass
 from collections.abc import Sequence
 from typing import Iterable, Mapping
 
+from itertools import repeat
+from operator import attrgetter
+
 import numpy as np
 
 from .. import _native
@@ -97,6 +100,8 @@ class SweepRow:
 
 
 _FOLD_FACTORS = {"none": (1, 1, 1), "2y": (1, 2, 1), "2z": (1, 1, 2)}
+_BLOCK_DIM = attrgetter("block_dim")
+_FOLDING = attrgetter("folding")
 
 
 # (family, template key) -> (template descriptor, context, template id):
@@ -149,17 +154,17 @@ class SweepPlan:
         folds = None
         if family.kind in ("stencil", "lbm") and len(tuple(family.grid)) == 3:
             try:
-                b = np.array([c.block_dim for c in configs], dtype=np.int64)
+                b = np.array(list(map(_BLOCK_DIM, configs)), dtype=np.int64)
                 ok_shape = b.shape == (n, 3)
             except (TypeError, ValueError):
                 ok_shape = False
             if ok_shape:
                 # foldings as codes into their distinct values (a handful per sweep)
-                folds = [c.folding for c in configs]
+                folds = list(map(_FOLDING, configs))
                 try:
                     ufolds = [f for f in dict.fromkeys(folds) if isinstance(f, str)]
                     ucode = {f: i for i, f in enumerate(ufolds)}
-                    fcode = np.array([ucode.get(f, -1) for f in folds], dtype=np.int64)
+                    fcode = np.array(list(map(ucode.get, folds, repeat(-1))), dtype=np.int64)
                 except TypeError:  # unhashable foldings: none of them is valid
                     ufolds = []
                     fcode = np.full(n, -1, dtype=np.int64)
@@ -201,7 +206,7 @@ class SweepPlan:
                 break
             block[i], grid[i], wpt[i], flops[i] = launch.block_dim, launch.grid_dim, launch.work_per_thread, fl
         idx = np.flatnonzero(keep)
-        self.configs = configs if len(idx) == n else [configs[i] for i in idx.tolist()]
+        self.configs = configs if len(idx) == n else list(map(configs.__getitem__, idx.tolist()))
         self.block, self.grid, self.wpt, self.flops = block[idx], grid[idx], wpt[idx], flops[idx]
         # one template per key (built from its first configuration), ids registered once
         self.templates: list = []
