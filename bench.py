@@ -382,7 +382,7 @@ def run_device(args, rank, world):
         "config": {"workload": WORKLOADS[args.workload], "configs_total": N,
                    "configs_per_rank_max": m, "parallelism": f"dp{world} (cost-dealt sharing-group shards, "
                    f"{'NCCL' if nccl or world == 1 else 'gloo'} all-gather + device rank)",
-                   "l2": "flushed between timed steps (256 MiB write)", "batch": int(os.environ.get("GVO_BATCH", 16384))},
+                   "l2": "flushed between timed steps (256 MiB write)", "batch": int(os.environ.get("GVO_BATCH", 65536))},
         "e2e": e2e,
         "gpu_launches": int(sum(kcnt[i] for i in range(5))),
         "launches_per_step": {k: v / max(1, args.steps) for k, v in launches.items()},

@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define GVO_ABI_VERSION 3
+#define GVO_ABI_VERSION 4
 
 /* ---- status codes: map 1:1 onto the reference's exception classes ---- */
 enum gvo_status {
@@ -365,6 +365,10 @@ int gvo_dedup_stats(gvo_ctx* ctx, int enable_counting, int64_t* shareable_units,
  * of configurations equal up to field-base translation and machine
  * capacities; GVO_PLAN_SHARE=0 turns that one off alone). */
 int gvo_set_dedup(gvo_ctx* ctx, int enable);
+/* Configurations per device batch for later calls on this context (plan ->
+ * sharing -> set kernel -> float assembly run batch by batch; default 65536,
+ * or GVO_BATCH at gvo_open).  Results do not depend on it. */
+int gvo_set_batch(gvo_ctx* ctx, int64_t configs_per_batch);
 /* Measured INT32 issue rate of the device (ops/s), the integer roofline. */
 int gvo_int_peak(gvo_ctx* ctx, double* ops_per_s);
 

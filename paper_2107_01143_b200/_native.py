@@ -21,7 +21,7 @@ _HERE = Path(__file__).resolve().parent
 _VARIANT = os.environ.get("GVO_LIB_VARIANT", "")
 LIB_PATH = _HERE / (f"libgvo_b200_{_VARIANT}.so" if _VARIANT else "libgvo_b200.so")
 
-ABI_VERSION = 3  # include/gvo_b200.h GVO_ABI_VERSION
+ABI_VERSION = 4  # include/gvo_b200.h GVO_ABI_VERSION
 GVO_MAX_FIELDS = 16
 GVO_MAX_ACCESSES = 1024
 GVO_MAX_BLOCK_SAMPLES = 32
@@ -162,6 +162,7 @@ def lib():
             "gvo_debug_units": (C.c_int, [P, C.c_int, P, i64, C.POINTER(C.c_int64)]),
             "gvo_dedup_stats": (C.c_int, [P, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
             "gvo_set_dedup": (C.c_int, [P, C.c_int]),
+            "gvo_set_batch": (C.c_int, [P, C.c_int64]),
             "gvo_format_ranking_csv": (C.c_int, [P, i64, P, C.c_char_p, P, i32, P, i64, C.POINTER(C.c_int64)]),
         }
         L.gvo_abi_version.restype = C.c_int
@@ -185,6 +186,7 @@ EXPORTED_SYMBOLS = (
     "gvo_rank", "gvo_sweep_host", "gvo_rank_gathered", "gvo_build_id", "gvo_sweep_host_ex", "gvo_group_footprint", "gvo_group_sets", "gvo_l1_cycles", "gvo_eval_addresses",
     "gvo_assemble_host", "gvo_predict_host", "gvo_set_timing", "gvo_kernel_times", "gvo_int_peak",
     "gvo_debug_units", "gvo_format_ranking_csv", "gvo_dedup_stats", "gvo_set_dedup",
+    "gvo_set_batch",
 )
 
 

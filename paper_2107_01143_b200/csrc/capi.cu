@@ -154,7 +154,7 @@ struct gvo_ctx {
   DBuf<double> s_stats, s_records, s_fd, s_gather;
   DBuf<int32_t> s_i32;
   DBuf<unsigned long long> s_ull;
-  int64_t batch = 16384;
+  int64_t batch = 65536;  // configurations per device batch (GVO_BATCH, gvo_set_batch)
   // optional per-kernel timing (CUDA events on the launching stream)
   bool timing = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
@@ -785,6 +785,12 @@ int gvo_dedup_stats(gvo_ctx* ctx, int enable_counting, int64_t* shareable_units,
   if (shareable_units) *shareable_units = ctx->dd_units;
   if (followers) *followers = ctx->dd_follow;
   return ctx->dedup ? 1 : 0;
+}
+
+int gvo_set_batch(gvo_ctx* ctx, int64_t configs_per_batch) {
+  if (!ctx || configs_per_batch < 1) return GVO_ERR_INVALID;
+  ctx->batch = configs_per_batch;
+  return GVO_OK;
 }
 
 int gvo_set_dedup(gvo_ctx* ctx, int enable) {

@@ -35,10 +35,20 @@ def _run(ctx, cfgs, on: bool):
     return out, units.value, follow.value
 
 
-def test_sharing_changes_nothing_on_structured_c5_slice():
+@pytest.fixture()
+def small_batches():
+    """Batches of 16,384 configurations for the test (the slice then spans
+    three batches: later batches copy from earlier ones), default after."""
+    ctx = _native.context()
+    ctx.check(_native.lib().gvo_set_batch(ctx.h, 16384))
+    yield ctx
+    ctx.check(_native.lib().gvo_set_batch(ctx.h, 65536))
+
+
+def test_sharing_changes_nothing_on_structured_c5_slice(small_batches):
     sp = _slice()
     assert len(sp) > 16384  # at least two batches: cross-batch sharing
-    ctx = _native.context()
+    ctx = small_batches
     cfgs = sp.config_array(ctx)
     try:
         off, _, f_off = _run(ctx, cfgs, False)
@@ -108,14 +118,14 @@ def test_plan_sharing_with_failing_leaders():
         assert np.array_equal(on[k].view(np.int64), off[k].view(np.int64)), k
 
 
-def test_pinned_sweep_host_pipelines_copies_identically():
+def test_pinned_sweep_host_pipelines_copies_identically(small_batches):
     """gvo_sweep_host_ex with page-locked outputs copies every batch to the
     host behind the next batches' kernels (a second stream); every output
     equals the pageable path's (one copy after the last batch)."""
     import torch
 
     sp = _slice()
-    ctx = _native.context()
+    ctx = small_batches
     cfgs = np.ascontiguousarray(sp.config_array(ctx))
     assert len(cfgs) > 16384
     ref = ctx.sweep_host(cfgs, 5, 2, 0)

@@ -103,7 +103,7 @@ def test_library_exports_every_header_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert declared <= set(_native.EXPORTED_SYMBOLS) | {"gvo_counts_stride"}
-    assert lib.gvo_abi_version() == _native.ABI_VERSION == 3
+    assert lib.gvo_abi_version() == _native.ABI_VERSION == 4
 
 
 def test_struct_layouts_match_header():
