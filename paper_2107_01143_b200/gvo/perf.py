@@ -151,6 +151,10 @@ class SweepPlan:
 
         tk = np.full(n, -1, dtype=np.int64)
         fast = np.zeros(n, dtype=bool)
+        # rejected by the vector check with every block extent >= 1 and a
+        # string folding: launch_of raises KernelError (a ValueError) for
+        # these, so a skip_invalid sweep skips them without the call
+        sure_bad = np.zeros(n, dtype=bool)
         folds = None
         if family.kind in ("stencil", "lbm") and len(tuple(family.grid)) == 3:
             try:
@@ -181,6 +185,7 @@ class SweepPlan:
                     ok &= ff.prod(axis=1) == 1  # lbm: folding "none" only
                     fl = 250 if family.flops_per_lup is None else family.flops_per_lup
                 fast = ok
+                sure_bad = ~ok & (b >= 1).all(axis=1) & (fcode >= 0) & (g >= 1).all()
                 block[ok] = b[ok]
                 grid[ok] = g[None, :] // np.where(eff[ok] > 0, eff[ok], 1)
                 wpt[ok] = ff[ok].prod(axis=1)
@@ -192,7 +197,9 @@ class SweepPlan:
                     tk[rows] = key_id(family.template_key(configs[int(np.argmax(rows))]))
         self.build_error = None  # (index, exception) of the first invalid config (skip_invalid=False)
         keep = np.ones(n, dtype=bool)
-        for i in np.flatnonzero(~fast):
+        if skip_invalid:
+            keep[sure_bad] = False
+        for i in np.flatnonzero(~fast & ~(sure_bad if skip_invalid else False)):
             cfg = configs[i]
             try:
                 launch, fl = family.launch_of(cfg)
