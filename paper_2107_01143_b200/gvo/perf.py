@@ -197,9 +197,11 @@ class SweepPlan:
                     tk[rows] = key_id(family.template_key(configs[int(np.argmax(rows))]))
         self.build_error = None  # (index, exception) of the first invalid config (skip_invalid=False)
         keep = np.ones(n, dtype=bool)
+        todo = ~fast
         if skip_invalid:
             keep[sure_bad] = False
-        for i in np.flatnonzero(~fast & ~(sure_bad if skip_invalid else False)):
+            todo &= ~sure_bad
+        for i in np.flatnonzero(todo):
             cfg = configs[i]
             try:
                 launch, fl = family.launch_of(cfg)
